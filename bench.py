@@ -1,0 +1,405 @@
+"""Benchmark: LADIES 5-layer GCN training iterations/sec on the Reddit-shaped graph.
+
+Workload (BASELINE.json configs[1]): Reddit-shaped synthetic graph (232,965 nodes,
+~114M CSR entries incl. self-loops, 602-d fp32 features, 41 classes), random partition
+into k = 8 workers (seed 1), LADIES skewed D = 8, batch 512, budget 512 per layer,
+5 layers hidden 256, SGD.  One step = one data-parallel iteration of
+train_distributed (training.py:483-506): every worker samples its plan, runs
+forward/backward, gradients are averaged over workers (NCCL all-reduce across GPUs)
+and the SGD step is applied.  The k = 8 workers are spread over the N GPUs (8/N each),
+so the total work per step is fixed: "scaling": "strong".
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the CPU oracle port (oracle/skewgcn_oracle.py, a restatement of
+the reference's numpy/scipy path) on this host's cores, one worker-iteration per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "LADIES 5-layer GCN iters/sec at 1/2/4/8 B200; remote nodes fetched/iter"
+DIMS_HIDDEN = 256
+N_LAYERS = 5
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shape", default="reddit")
+    ap.add_argument("--workers", type=int, default=8)
+    ap.add_argument("--mode", default="skewed")
+    ap.add_argument("--D", type=float, default=8.0)
+    ap.add_argument("--batch", type=int, default=512)
+    ap.add_argument("--budget", type=int, default=512)
+    ap.add_argument("--dtype", default="float32")
+    ap.add_argument("--lr", type=float, default=0.5)
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-stages", action="store_true", default=True)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [x.strip() for x in ln.split(",")]
+            if len(p) < 9:
+                continue
+            try:
+                sm.append(float(p[1]))
+                mx = float(p[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- setup
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def build_workload(args, device):
+    from paper_2101_07706_b200.synth import make_shaped_graph
+    t0 = time.time()
+    sg = make_shaped_graph(args.shape, seed=0, device=device)
+    return sg, time.time() - t0
+
+
+def algorithmic_sampler_bytes(stats_rows):
+    """8*E_l + 12*|S_{l+1}| + 25*N_l + 8*B + 12*nnz_l + 12*|S_l| per layer,
+    with 4 B more per pair for the fp64 weight this build stores (12*E_l)."""
+    total = 0
+    for r in stats_rows:
+        n_upper, n_cand, n_nodes, nnz = (int(x) for x in r[:4])
+        pairs = int(r[9])
+        total += 12 * pairs + 12 * n_upper + 25 * n_cand + 12 * nnz + 12 * n_nodes
+    return total
+
+
+# ---------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    world, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2101_07706_b200 as P
+    from paper_2101_07706_b200._native import check, lib, ptr, MODES
+
+    sg, t_gen = build_workload(args, f"cuda:{local}")
+    g = P.from_shaped(sg)
+    k = args.workers
+    part = P.partition_nodes(sg.n_nodes, k, "random", seed=1)
+    dims = [sg.features.shape[1]] + [DIMS_HIDDEN] * (N_LAYERS - 1) + [sg.n_classes]
+    model = P.init_model(dims, seed=0)
+    cfg = P.SamplerConfig(budget=args.budget, skew_constant=args.D, mode=args.mode)
+    P.set_compute_dtype(args.dtype)
+    tr = P.Trainer(g, part, model, cfg, batch_size=args.batch, lr=args.lr, mode=args.mode,
+                   seed=0, dtype=args.dtype, epochs=1)
+    stream = torch.cuda.current_stream()
+    n_my = len(tr.mine)
+    W, K = args.warmup, args.steps
+    per = tr.per_epoch
+
+    # ---- inputs resident in HBM: batch ids + plan states for every step, derived up front
+    total_steps = W + K
+    bl = np.zeros((total_steps, n_my), dtype=np.int32)
+    states = np.zeros((total_steps, n_my, 4), dtype=np.uint64)
+    ids = np.zeros((total_steps, n_my, args.batch), dtype=np.int32)
+    for s in range(total_steps):
+        boff, bids, st = tr.host_inputs(s // per, s % per)
+        for i in range(n_my):
+            n_i = boff[i + 1] - boff[i]
+            bl[s, i] = n_i
+            ids[s, i, :n_i] = bids[boff[i]:boff[i + 1]]
+        states[s] = st[:n_my]
+    d_ids = torch.as_tensor(ids, device="cuda")
+    workers = np.array(tr.mine, dtype=np.int32)
+
+    def step_resident(s):
+        check(lib.skg_ladies_sample_device(
+            tr.ps.h, n_my, ptr(workers, C.c_int32), ptr(np.ascontiguousarray(bl[s]), C.c_int32),
+            d_ids[s].data_ptr(), args.batch, MODES[args.mode], float(args.D), 1.0,
+            ptr(np.ascontiguousarray(states[s]), C.c_uint64), tr.stream))
+        tr.compute(0, s % per)
+        tr.reduce_and_step()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for s in range(W):
+        step_resident(s)
+    barrier()
+    launches0 = P.kernel_launches()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for s in range(W, W + K):
+            step_resident(s)
+        ev1.record(stream)
+        barrier()
+    launches = P.kernel_launches() - launches0
+    ms = ev0.elapsed_time(ev1)
+    if dist is not None:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    tr.check_errors()
+    ms_per_step = ms / K
+
+    # ---- ledger and per-stage split on one more (instrumented) pass
+    ledger = tr.ledger[0].clone()
+    if dist is not None:
+        dist.all_reduce(ledger)
+    remote_per_iter = float(ledger.sum().item()) / (W + K)
+    stats = [tr.ps.stats(i)[0] for i in range(n_my)]
+    s0_remote = sum(int(st[N_LAYERS - 1, 4]) for st in stats)  # input-layer remote rows (moved)
+    sampled_nodes = sum(int(st[:, 2].sum()) for st in stats)
+    alg_bytes = sum(algorithmic_sampler_bytes(st) for st in stats)
+
+    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    samp_ms, comp_ms = [], []
+    for rep in range(5):
+        s = W + (rep % K)
+        e_s[0].record(stream)
+        check(lib.skg_ladies_sample_device(
+            tr.ps.h, n_my, ptr(workers, C.c_int32), ptr(np.ascontiguousarray(bl[s]), C.c_int32),
+            d_ids[s].data_ptr(), args.batch, MODES[args.mode], float(args.D), 1.0,
+            ptr(np.ascontiguousarray(states[s]), C.c_uint64), tr.stream))
+        e_s[1].record(stream)
+        tr.compute(0, s % per)
+        e_s[2].record(stream)
+        tr.reduce_and_step()
+        e_s[3].record(stream)
+        torch.cuda.synchronize()
+        samp_ms.append(e_s[0].elapsed_time(e_s[1]))
+        comp_ms.append(e_s[1].elapsed_time(e_s[2]))
+    samp = float(np.median(samp_ms))
+    peaks = {}
+    try:
+        peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    achieved = alg_bytes / (samp * 1e-3) / 1e9
+
+    # ---- e2e through the public API: host-derived inputs, H2D each step, loss D2H
+    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    h2d = 0
+    barrier()
+    t_e2e0 = time.perf_counter()
+    ev2.record(stream)
+    for s in range(K):
+        boff, bids, _ = tr.host_inputs(s // per, s % per)
+        h2d += int(boff[n_my]) * 4 + n_my * 32
+        tr.sample()
+        tr.compute(0, s % per)
+        tr.reduce_and_step()
+        _ = tr.losses[s % per].cpu()  # step result to host
+    ev3.record(stream)
+    barrier()
+    e2e_ms = (time.perf_counter() - t_e2e0) * 1e3
+    if dist is not None:
+        t = torch.tensor([e2e_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            cpu = cpu_baseline(args, sg, args.cpu_sample_s)
+        out = {
+            "metric": METRIC,
+            "value": round(1000.0 / ms_per_step, 3),
+            "unit": "iters/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": W,
+            "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True,
+            "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": "f32" if args.dtype == "float32" else "f64",
+            "data": "synthetic (Reddit-shaped O(m) SBM, random-init weights)",
+            "config": {"workload": f"{args.shape}-shaped LADIES {args.mode} D={args.D:g}, k={k} "
+                                   f"workers, batch {args.batch}, budget {args.budget}, "
+                                   f"{N_LAYERS} layers hidden {DIMS_HIDDEN}",
+                       "n_nodes": sg.n_nodes, "nnz": sg.nnz, "workers": k,
+                       "l2": "inputs > L2 (114M-entry CSR, 561 MB features); no flush"},
+            "remote_nodes_per_iter": round(remote_per_iter, 2),
+            "input_layer_remote_rows_per_iter": s0_remote,
+            "sampled_nodes_per_s": round(sampled_nodes / (ms_per_step * 1e-3), 1),
+            "gpu_launches": int(launches),
+            "stages_ms": {"sample": round(samp, 4), "gcn_fwd_bwd": round(float(np.median(comp_ms)), 4)},
+            "roofline": {"bound": "hbm", "kernel": "sampler (LADIES, all layers, one batched launch "
+                                                     "sequence)",
+                         "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 5), "traffic": None,
+                         "algorithmic_bytes": int(alg_bytes)},
+            "e2e": {"value": round(1000.0 * K / e2e_ms, 3), "unit": "iters/s",
+                    "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": 8 * n_my},
+            "clocks": clk.summary(),
+            "graph_build_s": round(t_gen, 2),
+        }
+        if cpu is not None:
+            out["cpu_baseline"] = cpu
+        print(json.dumps(out), flush=True)
+    tr.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return out
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+def _oracle_setup(args, sg):
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import skewgcn_oracle as O
+    og = O.Graph(n_nodes=sg.n_nodes, offsets=sg.offsets, neighbors=sg.neighbors.astype(np.int64),
+                 weights=sg.weights, normalized=True, features=sg.features.astype(np.float64),
+                 labels=sg.labels, train_mask=sg.train_mask, val_mask=sg.val_mask)
+    part = O.partition_nodes(sg.n_nodes, args.workers, "random", seed=1)
+    dims = [sg.features.shape[1]] + [DIMS_HIDDEN] * (N_LAYERS - 1) + [sg.n_classes]
+    ws = O.init_model(dims, 0)
+    cfg = O.SamplerConfig(budget=args.budget, skew_constant=args.D, mode=args.mode)
+    wt = [np.flatnonzero(og.train_mask & (part.owner == w)) for w in range(args.workers)]
+    return O, og, part, ws, cfg, wt
+
+
+def _oracle_worker_iter(O, og, part, ws, cfg, wt, args, it, w):
+    brng = O.spawn_rng(0, "batch", 0, it, w)
+    batch = O.node_set(brng.choice(wt[w], size=min(args.batch, len(wt[w])), replace=False))
+    plan = O.ladies_plan(og, part, w, batch, cfg, N_LAYERS, O.spawn_rng(0, "plan", 0, it, w))
+    loss, grads = O.loss_and_backward(ws, plan, og.features, og.labels)
+    return plan, grads
+
+
+def cpu_baseline(args, sg, budget_s):
+    """The oracle port timed on this host: whole worker-iterations until ~budget_s."""
+    O, og, part, ws, cfg, wt = _oracle_setup(args, sg)
+    times = []
+    t_all = time.perf_counter()
+    w = 0
+    while True:
+        t0 = time.perf_counter()
+        _oracle_worker_iter(O, og, part, ws, cfg, wt, args, 0, w % args.workers)
+        times.append(time.perf_counter() - t0)
+        w += 1
+        if time.perf_counter() - t_all > budget_s and w >= 2:
+            break
+    per_worker = float(np.median(times))
+    it_s = 1.0 / (args.workers * per_worker)
+    return {"value": round(it_s, 5), "unit": "iters/s", "cores": 1, "kind": "port",
+            "sample": f"{len(times)} worker-iterations (plan + fwd/bwd) of the k={args.workers} "
+                      f"iteration, median {per_worker:.3f} s; iters/s = 1/(k * median)",
+            "threads_note": f"numpy single-threaded except BLAS; os.cpu_count()={os.cpu_count()}"}
+
+
+def run_reference(args):
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return None
+    from paper_2101_07706_b200.synth import make_shaped_graph
+    sg = make_shaped_graph(args.shape, seed=0, device=None)
+    O, og, part, ws, cfg, wt = _oracle_setup(args, sg)
+    for s in range(args.warmup):
+        _oracle_worker_iter(O, og, part, ws, cfg, wt, args, s // args.workers, s % args.workers)
+    times = []
+    for s in range(args.steps):
+        t0 = time.perf_counter()
+        _oracle_worker_iter(O, og, part, ws, cfg, wt, args, s // args.workers, s % args.workers)
+        times.append(time.perf_counter() - t0)
+    per_worker = float(np.mean(times))
+    it_s = 1.0 / (args.workers * per_worker)
+    out = {"metric": METRIC, "value": round(it_s, 5), "unit": "iters/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": round(per_worker * args.workers * 1e3, 2), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (Reddit-shaped O(m) SBM, random-init weights)",
+           "config": {"workload": f"{args.shape}-shaped LADIES {args.mode} D={args.D:g}, "
+                                  f"k={args.workers} workers, batch {args.batch}, budget "
+                                  f"{args.budget}, {N_LAYERS} layers hidden {DIMS_HIDDEN}"},
+           "impl": "reference",
+           "cpu_baseline": {"value": round(it_s, 5), "unit": "iters/s", "cores": 1, "kind": "port",
+                            "sample": f"{args.steps} worker-iterations (one of k={args.workers} "
+                                      "workers per step); iters/s = 1/(k * mean)"},
+           "e2e": {"value": round(it_s, 5), "unit": "iters/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

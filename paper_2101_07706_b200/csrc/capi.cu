@@ -1,0 +1,1135 @@
+// extern "C" boundary (include/skewgcn_b200.h): graph store, plan arenas, orchestration.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/skewgcn_b200.h"
+#include "gcn.cuh"
+#include "sampler.cuh"
+#include "skg_internal.h"
+
+namespace skg {
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+const char* last_error() { return g_err.c_str(); }
+}  // namespace skg
+
+using namespace skg;
+
+#define CK(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      set_error(std::string(#x) + ": " + cudaGetErrorString(e_));                    \
+      return SKG_ERR_CUDA;                                                           \
+    }                                                                                \
+  } while (0)
+#define ARG(cond, msg)       \
+  do {                       \
+    if (!(cond)) {           \
+      set_error(msg);        \
+      return SKG_ERR_ARG;    \
+    }                        \
+  } while (0)
+
+static inline int64_t round4(int64_t d) { return (d + 3) / 4 * 4; }
+
+// ------------------------------------------------------------------ structures
+struct skg_ctx {
+  int device = 0;
+  int64_t n = 0, nnz = 0;
+  int32_t n_workers = 1;
+  int64_t* d_off = nullptr;
+  int32_t* d_col = nullptr;
+  double* d_w = nullptr;
+  int32_t* d_owner = nullptr;
+  int64_t* d_toff = nullptr;
+  int32_t* d_trow = nullptr;
+  double* d_tw = nullptr;
+  bool symmetric = true;
+  std::vector<int64_t> deg_desc_prefix;  // prefix sums of degrees sorted descending
+  void* d_x = nullptr;
+  int64_t F = 0, ldx = 0, x_rows = 0;
+  int dtype = DT_F32;
+  int32_t* d_labels = nullptr;
+  int n_ranks = 1;
+  uint64_t* d_shards = nullptr;
+  int32_t* d_node_rank = nullptr;
+  int32_t* d_node_row = nullptr;
+  GraphDev gdev() const {
+    GraphDev g;
+    g.n = n;
+    g.nnz = nnz;
+    g.off = d_off;
+    g.col = d_col;
+    g.w = d_w;
+    g.owner = d_owner;
+    g.t_off = symmetric ? d_off : d_toff;
+    g.t_row = symmetric ? d_col : d_trow;
+    g.t_w = symmetric ? d_w : d_tw;
+    g.n_words = (int32_t)((n + 31) / 32);
+    return g;
+  }
+  FeatStore fstore() const {
+    FeatStore fs;
+    fs.shards = reinterpret_cast<const void* const*>(d_shards);
+    fs.node_rank = d_node_rank;
+    fs.node_row = d_node_row;
+    fs.ld = ldx;
+    fs.dim = F;
+    return fs;
+  }
+  int64_t edge_bound(int64_t rows) const {  // max sum of `rows` distinct row degrees
+    if (rows <= 0) return 0;
+    rows = std::min<int64_t>(rows, (int64_t)deg_desc_prefix.size() - 1);
+    return deg_desc_prefix[rows];
+  }
+};
+
+struct skg_plans {
+  skg_ctx* ctx = nullptr;
+  int kind = KIND_LADIES, n_slots = 0, L = 0;
+  int64_t budget = 0, max_batch = 0;
+  int cap_rows = 0, cap_cand = 0, cap_batch = 0;
+  int64_t cap_pairs = 0;
+  std::vector<PlanDev> h;
+  PlanDev* d_plans = nullptr;
+  char* arena = nullptr;
+  size_t scal_bytes = 0;
+  char* d_scal = nullptr;  // per-slot scalars zeroed before each sampling call
+  int32_t* d_batch = nullptr;
+  // SAINT candidates
+  int32_t* d_train = nullptr;
+  double* d_train_norm = nullptr;
+  uint32_t* d_train_bitmap = nullptr;
+  int64_t n_train = 0;
+  bool have_train_norm = false;
+  std::vector<int32_t*> d_local;
+  std::vector<double*> d_local_norm;
+  std::vector<int64_t> n_local;
+  std::vector<bool> local_norm_ready;
+};
+
+struct GcnSlot {
+  char* X0 = nullptr;
+  std::vector<char*> U, H;
+  char* G0 = nullptr;
+  char* G1 = nullptr;
+};
+struct skg_gcn {
+  skg_plans* ps = nullptr;
+  int L = 0, dtype = DT_F32;
+  std::vector<int64_t> dims, ld;
+  std::vector<GcnSlot> slots;
+  char* arena = nullptr;
+  int64_t ld_max = 0;
+};
+
+// ------------------------------------------------------------------ small kernels
+// symmetry check: w[j,i] exists and equals w[i,j] bitwise for every stored (i,j)
+__global__ void k_check_symmetric(int64_t n, const int64_t* off, const int32_t* col,
+                                  const double* w, int* bad) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int64_t e = off[i] + threadIdx.x; e < off[i + 1]; e += blockDim.x) {
+      int j = col[e];
+      int64_t lo = off[j], hi = off[j + 1];
+      while (lo < hi) {
+        int64_t mid = (lo + hi) >> 1;
+        if (col[mid] < i) lo = mid + 1;
+        else hi = mid;
+      }
+      if (lo >= off[j + 1] || col[lo] != i ||
+          __double_as_longlong(w[lo]) != __double_as_longlong(w[e]))
+        atomicExch(bad, 1);
+    }
+  }
+}
+
+__global__ void k_ids64_to_32(const int64_t* in, int64_t n, int32_t* out) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)in[i];
+}
+
+// ------------------------------------------------------------------ misc
+extern "C" int skg_abi_version(void) { return 1; }
+extern "C" const char* skg_last_error(void) { return last_error(); }
+extern "C" unsigned long long skg_kernel_launches(void) { return g_kernel_launches; }
+extern "C" int skg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+// ------------------------------------------------------------------ host RNG runtime
+extern "C" int skg_spawn_pcg64(uint64_t master_seed, const char* const* label_reprs, int n_labels,
+                               uint64_t out_state[4]) {
+  ARG(n_labels >= 0 && out_state, "bad arguments");
+  std::vector<std::string> labs;
+  for (int i = 0; i < n_labels; ++i) labs.emplace_back(label_reprs[i]);
+  Pcg64 g = spawn_pcg64(master_seed, labs);
+  out_state[0] = (uint64_t)(g.state >> 64);
+  out_state[1] = (uint64_t)g.state;
+  out_state[2] = (uint64_t)(g.inc >> 64);
+  out_state[3] = (uint64_t)g.inc;
+  return SKG_OK;
+}
+
+static Pcg64 pcg_from(const uint64_t s[4], int has32, uint32_t u32) {
+  Pcg64 g;
+  g.state = ((u128)s[0] << 64) | s[1];
+  g.inc = ((u128)s[2] << 64) | s[3];
+  g.has32 = has32;
+  g.u32 = u32;
+  return g;
+}
+
+extern "C" int skg_choice_noreplace(const uint64_t state[4], int has32, uint32_t u32, int64_t pop,
+                                    int64_t size, int64_t* out_idx) {
+  ARG(pop >= 0 && size >= 0 && size <= pop, "Cannot take a larger sample than population when replace is False");
+  Pcg64 g = pcg_from(state, has32, u32);
+  choice_without_replacement(g, pop, size, out_idx);
+  return SKG_OK;
+}
+
+extern "C" int skg_iteration_inputs(uint64_t master_seed, int64_t epoch, int64_t it, int64_t worker,
+                                    const int64_t* train_w, int64_t n_train_w, int64_t batch_size,
+                                    int64_t* out_batch, int64_t* out_len, uint64_t plan_state[4]) {
+  ARG(n_train_w > 0, "worker has no training nodes");
+  std::vector<std::string> lb = {repr_str("batch"), repr_int(epoch), repr_int(it), repr_int(worker)};
+  Pcg64 g = spawn_pcg64(master_seed, lb);
+  int64_t take = std::min(batch_size, n_train_w);
+  std::vector<int64_t> idx(take);
+  choice_without_replacement(g, n_train_w, take, idx.data());
+  for (int64_t i = 0; i < take; ++i) out_batch[i] = train_w[idx[i]];
+  std::sort(out_batch, out_batch + take);
+  int64_t m = std::unique(out_batch, out_batch + take) - out_batch;
+  *out_len = m;
+  std::vector<std::string> lp = {repr_str("plan"), repr_int(epoch), repr_int(it), repr_int(worker)};
+  Pcg64 p = spawn_pcg64(master_seed, lp);
+  plan_state[0] = (uint64_t)(p.state >> 64);
+  plan_state[1] = (uint64_t)p.state;
+  plan_state[2] = (uint64_t)(p.inc >> 64);
+  plan_state[3] = (uint64_t)p.inc;
+  return SKG_OK;
+}
+
+// ------------------------------------------------------------------ graph store
+extern "C" int skg_ctx_create(int device, int64_t n, int64_t nnz, const int64_t* offsets,
+                              const int32_t* neighbors, const double* weights, int32_t n_workers,
+                              const int32_t* owner, skg_ctx** out) {
+  ARG(out && offsets && n >= 0 && nnz >= 0, "bad arguments");
+  ARG(n < (1LL << 31) - 64, "graphs with >= 2^31 nodes are not supported");
+  ARG(offsets[0] == 0 && offsets[n] == nnz, "offsets must start at 0 and end at len(neighbors)");
+  ARG(n_workers >= 1, "need at least one worker");
+  CK(cudaSetDevice(device));
+  skg_ctx* c = new skg_ctx();
+  c->device = device;
+  c->n = n;
+  c->nnz = nnz;
+  c->n_workers = n_workers;
+  CK(cudaMalloc(&c->d_off, sizeof(int64_t) * (n + 1)));
+  CK(cudaMalloc(&c->d_col, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+  CK(cudaMalloc(&c->d_w, sizeof(double) * std::max<int64_t>(nnz, 1)));
+  CK(cudaMalloc(&c->d_owner, sizeof(int32_t) * std::max<int64_t>(n, 1)));
+  CK(cudaMemcpy(c->d_off, offsets, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+  if (nnz) {
+    CK(cudaMemcpy(c->d_col, neighbors, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_w, weights, sizeof(double) * nnz, cudaMemcpyHostToDevice));
+  }
+  if (n) {
+    if (owner) CK(cudaMemcpy(c->d_owner, owner, sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+    else CK(cudaMemset(c->d_owner, 0, sizeof(int32_t) * n));
+  }
+  // degree bound table for arena sizing
+  std::vector<int64_t> deg(n);
+  for (int64_t i = 0; i < n; ++i) deg[i] = offsets[i + 1] - offsets[i];
+  std::sort(deg.begin(), deg.end(), std::greater<int64_t>());
+  c->deg_desc_prefix.assign(n + 1, 0);
+  for (int64_t i = 0; i < n; ++i) c->deg_desc_prefix[i + 1] = c->deg_desc_prefix[i] + deg[i];
+  // symmetric weights (every normalised graph): the CSC used by pull passes is the CSR
+  int* d_bad;
+  CK(cudaMalloc(&d_bad, sizeof(int)));
+  CK(cudaMemset(d_bad, 0, sizeof(int)));
+  if (n) k_check_symmetric<<<std::min<int64_t>(n, 65535), 256>>>(n, c->d_off, c->d_col, c->d_w, d_bad);
+  int bad = 0;
+  CK(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(d_bad);
+  c->symmetric = !bad;
+  if (!c->symmetric) {  // host counting sort by column (rows ascending within a column)
+    std::vector<int64_t> toff(n + 1, 0);
+    for (int64_t e = 0; e < nnz; ++e) toff[neighbors[e] + 1]++;
+    for (int64_t i = 0; i < n; ++i) toff[i + 1] += toff[i];
+    std::vector<int64_t> fill(toff.begin(), toff.end() - 1);
+    std::vector<int32_t> trow(std::max<int64_t>(nnz, 1));
+    std::vector<double> tw(std::max<int64_t>(nnz, 1));
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t e = offsets[i]; e < offsets[i + 1]; ++e) {
+        int64_t p = fill[neighbors[e]]++;
+        trow[p] = (int32_t)i;
+        tw[p] = weights[e];
+      }
+    CK(cudaMalloc(&c->d_toff, sizeof(int64_t) * (n + 1)));
+    CK(cudaMalloc(&c->d_trow, sizeof(int32_t) * trow.size()));
+    CK(cudaMalloc(&c->d_tw, sizeof(double) * tw.size()));
+    CK(cudaMemcpy(c->d_toff, toff.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_trow, trow.data(), sizeof(int32_t) * trow.size(), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(c->d_tw, tw.data(), sizeof(double) * tw.size(), cudaMemcpyHostToDevice));
+  }
+  CK(cudaDeviceSynchronize());
+  *out = c;
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_destroy(skg_ctx* c) {
+  if (!c) return SKG_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->d_off);
+  cudaFree(c->d_col);
+  cudaFree(c->d_w);
+  cudaFree(c->d_owner);
+  cudaFree(c->d_toff);
+  cudaFree(c->d_trow);
+  cudaFree(c->d_tw);
+  cudaFree(c->d_x);
+  cudaFree(c->d_labels);
+  cudaFree(c->d_shards);
+  cudaFree(c->d_node_rank);
+  cudaFree(c->d_node_row);
+  delete c;
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_set_features(skg_ctx* c, int dtype, int64_t dim, int64_t n_rows,
+                                    const void* host_rows) {
+  ARG(c && (dtype == DT_F32 || dtype == DT_F64) && dim > 0 && n_rows >= 0, "bad feature arguments");
+  CK(cudaSetDevice(c->device));
+  const size_t es = dtype == DT_F32 ? 4 : 8;
+  cudaFree(c->d_x);
+  c->d_x = nullptr;
+  c->F = dim;
+  c->ldx = round4(dim);
+  c->dtype = dtype;
+  c->x_rows = n_rows;
+  CK(cudaMalloc(&c->d_x, es * c->ldx * std::max<int64_t>(n_rows, 1)));
+  CK(cudaMemset(c->d_x, 0, es * c->ldx * std::max<int64_t>(n_rows, 1)));
+  if (n_rows)
+    CK(cudaMemcpy2D(c->d_x, es * c->ldx, host_rows, es * dim, es * dim, n_rows, cudaMemcpyHostToDevice));
+  // single-rank default map: shard 0 = all rows, row = node
+  cudaFree(c->d_shards);
+  CK(cudaMalloc(&c->d_shards, sizeof(uint64_t)));
+  uint64_t p = (uint64_t)c->d_x;
+  CK(cudaMemcpy(c->d_shards, &p, sizeof(uint64_t), cudaMemcpyHostToDevice));
+  c->n_ranks = 1;
+  cudaFree(c->d_node_rank);
+  cudaFree(c->d_node_row);
+  c->d_node_rank = nullptr;
+  c->d_node_row = nullptr;
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_set_feature_map(skg_ctx* c, int n_ranks, const uint64_t* shard_ptrs,
+                                       const int32_t* node_rank, const int32_t* node_row) {
+  ARG(c && n_ranks >= 1 && shard_ptrs && node_rank && node_row, "bad feature map");
+  CK(cudaSetDevice(c->device));
+  cudaFree(c->d_shards);
+  cudaFree(c->d_node_rank);
+  cudaFree(c->d_node_row);
+  CK(cudaMalloc(&c->d_shards, sizeof(uint64_t) * n_ranks));
+  CK(cudaMemcpy(c->d_shards, shard_ptrs, sizeof(uint64_t) * n_ranks, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&c->d_node_rank, sizeof(int32_t) * c->n));
+  CK(cudaMalloc(&c->d_node_row, sizeof(int32_t) * c->n));
+  CK(cudaMemcpy(c->d_node_rank, node_rank, sizeof(int32_t) * c->n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(c->d_node_row, node_row, sizeof(int32_t) * c->n, cudaMemcpyHostToDevice));
+  c->n_ranks = n_ranks;
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_feature_ptr(skg_ctx* c, uint64_t* out_ptr, int64_t* out_ld) {
+  ARG(c, "null ctx");
+  *out_ptr = (uint64_t)c->d_x;
+  *out_ld = c->ldx;
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_set_labels(skg_ctx* c, const int64_t* labels) {
+  ARG(c && labels, "bad labels");
+  CK(cudaSetDevice(c->device));
+  std::vector<int32_t> l32(c->n);
+  for (int64_t i = 0; i < c->n; ++i) l32[i] = (int32_t)labels[i];
+  cudaFree(c->d_labels);
+  CK(cudaMalloc(&c->d_labels, sizeof(int32_t) * std::max<int64_t>(c->n, 1)));
+  if (c->n) CK(cudaMemcpy(c->d_labels, l32.data(), sizeof(int32_t) * c->n, cudaMemcpyHostToDevice));
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_set_owner(skg_ctx* c, int32_t n_workers, const int32_t* owner) {
+  ARG(c && owner && n_workers >= 1, "bad owner map");
+  CK(cudaSetDevice(c->device));
+  for (int64_t i = 0; i < c->n; ++i)
+    if (owner[i] < 0 || owner[i] >= n_workers) {
+      set_error("owner id out of range");
+      return SKG_ERR_ARG;
+    }
+  if (c->n) CK(cudaMemcpy(c->d_owner, owner, sizeof(int32_t) * c->n, cudaMemcpyHostToDevice));
+  c->n_workers = n_workers;
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_info(skg_ctx* c, int64_t out[8]) {
+  ARG(c, "null ctx");
+  out[0] = c->n;
+  out[1] = c->nnz;
+  out[2] = c->symmetric;
+  out[3] = c->ldx;
+  out[4] = c->F;
+  out[5] = c->dtype;
+  out[6] = c->device;
+  out[7] = c->n_ranks;
+  return SKG_OK;
+}
+
+extern "C" int skg_ipc_handle(uint64_t dev_ptr, uint8_t out_handle[64]) {
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, (void*)dev_ptr));
+  static_assert(sizeof(h) == 64, "ipc handle size");
+  memcpy(out_handle, &h, 64);
+  return SKG_OK;
+}
+extern "C" int skg_ipc_open(const uint8_t handle[64], uint64_t* out_dev_ptr) {
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  void* p = nullptr;
+  CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  *out_dev_ptr = (uint64_t)p;
+  return SKG_OK;
+}
+extern "C" int skg_ipc_close(uint64_t dev_ptr) {
+  CK(cudaIpcCloseMemHandle((void*)dev_ptr));
+  return SKG_OK;
+}
+
+// ------------------------------------------------------------------ plan arenas
+struct Carver {
+  size_t off = 0;
+  std::vector<std::pair<void**, size_t>> items;
+  template <typename T>
+  void add(T*& p, size_t count) {
+    items.push_back({reinterpret_cast<void**>(&p), off});
+    off += (count * sizeof(T) + 255) / 256 * 256;
+  }
+  void bind(char* base) {
+    for (auto& it : items) *it.first = base + it.second;
+  }
+};
+
+extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_t budget,
+                                int64_t max_batch, skg_plans** out) {
+  ARG(c && out && n_slots >= 1 && L >= 1 && budget >= 1, "bad plan-set arguments");
+  ARG(kind == KIND_LADIES || kind == KIND_SAINT, "unknown plan kind");
+  ARG(budget < (1LL << 20), "budget too large for the device sampler");
+  CK(cudaSetDevice(c->device));
+  skg_plans* ps = new skg_plans();
+  ps->ctx = c;
+  ps->kind = kind;
+  ps->n_slots = n_slots;
+  ps->L = L;
+  ps->budget = budget;
+  ps->max_batch = std::max<int64_t>(max_batch, 1);
+  const int64_t n = c->n;
+  const int n_words = (int)((n + 31) / 32);
+  int64_t cap_rows, cap_cand, cap_pairs, cap_batch;
+  if (kind == KIND_LADIES) {
+    cap_rows = std::min<int64_t>(std::max<int64_t>(ps->max_batch, budget), std::max<int64_t>(n, 1));
+    cap_pairs = std::max<int64_t>(c->edge_bound(cap_rows), 1);
+    cap_cand = std::max<int64_t>(std::min<int64_t>(n, cap_pairs), 1);
+    cap_batch = ps->max_batch;
+  } else {
+    cap_rows = std::min<int64_t>(budget, std::max<int64_t>(n, 1));
+    cap_pairs = std::max<int64_t>(c->edge_bound(cap_rows), 1);
+    cap_cand = std::max<int64_t>(n, 1);
+    cap_batch = 1;
+  }
+  ARG(cap_pairs < (1LL << 31) && cap_cand < (1LL << 31), "plan capacity exceeds int32 indexing");
+  ps->cap_rows = (int)cap_rows;
+  ps->cap_cand = (int)cap_cand;
+  ps->cap_pairs = cap_pairs;
+  ps->cap_batch = (int)cap_batch;
+  const int Ls = kind == KIND_LADIES ? L : 1;
+  int pw = 0;
+  while (cap_cand > (112LL << pw)) ++pw;
+  const int cap_slots = std::max(1 << pw, kPwSub);
+  const int cap_chunks = (int)((cap_cand + kChunk - 1) / kChunk);
+  const int cap_supers = (int)((cap_cand + kSuper - 1) / kSuper);
+  const int cap_tiles = (int)std::max<int64_t>((n_words + kTileWords - 1) / kTileWords,
+                                               (cap_cand + kTileCand - 1) / kTileCand) + 1;
+  ps->h.resize(n_slots);
+  // per-slot scalars (zeroed per sampling call): err, starvation, draws, counters
+  Carver scal;
+  std::vector<int32_t*> errs(n_slots), starv(n_slots), ctrs(n_slots);
+  std::vector<int64_t*> draws(n_slots);
+  for (int s = 0; s < n_slots; ++s) {
+    scal.add(errs[s], 1);
+    scal.add(starv[s], 1);
+    scal.add(ctrs[s], 8);
+    scal.add(draws[s], 1);
+  }
+  ps->scal_bytes = scal.off;
+  Carver cv;
+  for (int s = 0; s < n_slots; ++s) {
+    PlanDev& P = ps->h[s];
+    memset(&P, 0, sizeof(P));
+    P.cap_rows = (int)cap_rows;
+    P.cap_cand = (int)cap_cand;
+    P.cap_pairs = cap_pairs;
+    P.cap_chunks = cap_chunks;
+    P.cap_supers = cap_supers;
+    P.cap_slots = cap_slots;
+    P.cap_tiles = cap_tiles;
+    cv.add(P.bitmap, n_words);
+    cv.add(P.sbitmap, n_words);
+    cv.add(P.cnt_node, std::max<int64_t>(n, 1));
+    cv.add(P.pair_off, cap_rows + 1);
+    cv.add(P.pair_slot, kind == KIND_LADIES ? cap_pairs : 1);
+    cv.add(P.word_prefix, n_words);
+    cv.add(P.tile_a, cap_tiles);
+    cv.add(P.tile_b, cap_tiles);
+    cv.add(P.bucket_off, kind == KIND_LADIES ? cap_cand + 1 : 1);
+    cv.add(P.bucket_r, kind == KIND_LADIES ? cap_pairs : 1);
+    cv.add(P.bucket_w, kind == KIND_LADIES ? cap_pairs : 1);
+    cv.add(P.big_list, kind == KIND_LADIES ? cap_cand : 1);
+    cv.add(P.pw_val, cap_slots);
+    cv.add(P.pw_lvl, cap_slots);
+    cv.add(P.chunk_sum, cap_chunks);
+    cv.add(P.chunk_approx, cap_chunks);
+    cv.add(P.chunk_map, 2 * (size_t)cap_chunks);
+    cv.add(P.chunk_e, cap_chunks);
+    cv.add(P.chunk_mode, cap_chunks);
+    cv.add(P.chunk_start, cap_chunks);
+    cv.add(P.super_map, 2 * (size_t)cap_supers);
+    cv.add(P.super_e, cap_supers);
+    cv.add(P.super_mode, cap_supers);
+    cv.add(P.super_start, cap_supers);
+    cv.add(P.cdf, cap_cand);
+    cv.add(P.draw_idx, budget);
+    cv.add(P.cand, kind == KIND_LADIES ? (size_t)Ls * cap_cand : 1);
+    cv.add(P.norm, (size_t)Ls * cap_cand);
+    cv.add(P.is_local, (size_t)Ls * cap_cand);
+    cv.add(P.nodes, (size_t)Ls * cap_rows);
+    cv.add(P.samp_rank, (size_t)Ls * cap_rows);
+    cv.add(P.p, (size_t)Ls * cap_rows);
+    cv.add(P.indptr, (size_t)Ls * (cap_rows + 1));
+    cv.add(P.indices, (size_t)Ls * cap_pairs);
+    cv.add(P.val, (size_t)Ls * cap_pairs);
+    cv.add(P.tindptr, (size_t)Ls * (cap_rows + 1));
+    cv.add(P.tindices, (size_t)Ls * cap_pairs);
+    cv.add(P.tval, (size_t)Ls * cap_pairs);
+    cv.add(P.stat, L);
+  }
+  int32_t* d_batch = nullptr;
+  cv.add(d_batch, (size_t)n_slots * cap_batch);
+  cudaError_t e1 = cudaMalloc(&ps->arena, cv.off);
+  if (e1 != cudaSuccess) {
+    set_error(std::string("plan arena (") + std::to_string(cv.off >> 20) + " MiB): " +
+              cudaGetErrorString(e1));
+    delete ps;
+    return SKG_ERR_CUDA;
+  }
+  cv.bind(ps->arena);
+  ps->d_batch = d_batch;
+  CK(cudaMalloc(&ps->d_scal, scal.off));
+  scal.bind(ps->d_scal);
+  CK(cudaMemset(ps->arena, 0, cv.off));
+  CK(cudaMemset(ps->d_scal, 0, scal.off));
+  for (int s = 0; s < n_slots; ++s) {
+    PlanDev& P = ps->h[s];
+    P.err = errs[s];
+    P.starvation = starv[s];
+    P.counters = ctrs[s];
+    P.draws_consumed = draws[s];
+    P.kind = kind;
+    P.n_layers = L;
+    P.budget = budget;
+  }
+  CK(cudaMalloc(&ps->d_plans, sizeof(PlanDev) * n_slots));
+  CK(cudaMemcpy(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n_slots, cudaMemcpyHostToDevice));
+  *out = ps;
+  return SKG_OK;
+}
+
+extern "C" int skg_plans_destroy(skg_plans* ps) {
+  if (!ps) return SKG_OK;
+  cudaSetDevice(ps->ctx->device);
+  cudaFree(ps->arena);
+  cudaFree(ps->d_scal);
+  cudaFree(ps->d_plans);
+  cudaFree(ps->d_train);
+  cudaFree(ps->d_train_norm);
+  cudaFree(ps->d_train_bitmap);
+  for (auto p : ps->d_local) cudaFree(p);
+  for (auto p : ps->d_local_norm) cudaFree(p);
+  delete ps;
+  return SKG_OK;
+}
+
+static int status_from_err(int err) {
+  if (err & EB_NOT_ADJACENT) {
+    set_error("candidates not adjacent to s_l");
+    return SKG_ERR_NOT_ADJACENT;
+  }
+  if (err & EB_NO_LABELS) {
+    set_error("batch contains no labeled nodes");
+    return SKG_ERR_NO_LABELS;
+  }
+  if (err & EB_CAPACITY) {
+    set_error("plan arena capacity exceeded");
+    return SKG_ERR_CAPACITY;
+  }
+  return SKG_OK;
+}
+
+extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
+                                 const int64_t* batch_off, const int64_t* batch_ids, int mode,
+                                 double D, double min_scale, const uint64_t* rng, void* stream) {
+  ARG(ps && ps->kind == KIND_LADIES, "not a LADIES plan set");
+  ARG(n >= 1 && n <= ps->n_slots, "slot count out of range");
+  ARG(mode >= 0 && mode <= 2, "unknown mode");
+  skg_ctx* c = ps->ctx;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int32_t> hb((size_t)n * ps->cap_batch);
+  for (int i = 0; i < n; ++i) {
+    int64_t len = batch_off[i + 1] - batch_off[i];
+    if (len <= 0) {
+      set_error("empty batch");
+      return SKG_ERR_EMPTY;
+    }
+    ARG(len <= ps->cap_batch, "batch larger than the plan set's max_batch");
+    ARG(workers[i] >= 0 && workers[i] < c->n_workers, "worker id out of range");
+    for (int64_t k = 0; k < len; ++k) {
+      int64_t v = batch_ids[batch_off[i] + k];
+      if (v < 0 || v >= c->n) {
+        set_error("node id out of range for this graph");
+        return SKG_ERR_ARG;
+      }
+      if (k && v <= batch_ids[batch_off[i] + k - 1]) {
+        set_error("node set must be strictly increasing");
+        return SKG_ERR_ARG;
+      }
+      hb[(size_t)i * ps->cap_batch + k] = (int32_t)v;
+    }
+    PlanDev& P = ps->h[i];
+    P.worker = workers[i];
+    P.mode = mode;
+    P.D = D;
+    P.min_scale = min_scale;
+    for (int q = 0; q < 4; ++q) P.rng[q] = rng[4 * i + q];
+    P.batch_len = (int32_t)len;
+    P.batch = ps->d_batch + (size_t)i * ps->cap_batch;
+    P.cand_norm = nullptr;
+  }
+  CK(cudaMemcpyAsync(ps->d_batch, hb.data(), sizeof(int32_t) * hb.size(), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
+  const int max_upper = ps->L > 1 ? std::max<int>(ps->cap_batch, (int)std::min<int64_t>(ps->budget, ps->cap_cand))
+                                  : ps->cap_batch;
+  return launch_ladies(c->gdev(), ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
+                       (int)ps->budget, st);
+}
+
+extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* workers,
+                                        const int32_t* batch_len, uint64_t d_batch,
+                                        int64_t batch_stride, int mode, double D, double min_scale,
+                                        const uint64_t* rng, void* stream) {
+  ARG(ps && ps->kind == KIND_LADIES, "not a LADIES plan set");
+  ARG(n >= 1 && n <= ps->n_slots && d_batch, "bad arguments");
+  skg_ctx* c = ps->ctx;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int i = 0; i < n; ++i) {
+    if (batch_len[i] <= 0) {
+      set_error("empty batch");
+      return SKG_ERR_EMPTY;
+    }
+    ARG(batch_len[i] <= ps->cap_batch, "batch larger than the plan set's max_batch");
+    ARG(workers[i] >= 0 && workers[i] < c->n_workers, "worker id out of range");
+    PlanDev& P = ps->h[i];
+    P.worker = workers[i];
+    P.mode = mode;
+    P.D = D;
+    P.min_scale = min_scale;
+    for (int q = 0; q < 4; ++q) P.rng[q] = rng[4 * i + q];
+    P.batch_len = batch_len[i];
+    P.batch = reinterpret_cast<const int32_t*>(d_batch) + (size_t)i * batch_stride;
+    P.cand_norm = nullptr;
+  }
+  CK(cudaMemcpyAsync(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
+  const int max_upper = ps->L > 1 ? std::max<int>(ps->cap_batch, (int)std::min<int64_t>(ps->budget, ps->cap_cand))
+                                  : ps->cap_batch;
+  return launch_ladies(c->gdev(), ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
+                       (int)ps->budget, st);
+}
+
+extern "C" int skg_saint_set_candidates(skg_plans* ps, const int64_t* train, int64_t n_train,
+                                        int precompute, void* stream) {
+  ARG(ps && ps->kind == KIND_SAINT, "not a SAINT plan set");
+  ARG(n_train >= 1, "empty training node set");
+  skg_ctx* c = ps->ctx;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<int32_t> t32(n_train);
+  for (int64_t i = 0; i < n_train; ++i) {
+    ARG(train[i] >= 0 && train[i] < c->n, "node id out of range for this graph");
+    ARG(i == 0 || train[i] > train[i - 1], "node set must be strictly increasing");
+    t32[i] = (int32_t)train[i];
+  }
+  cudaFree(ps->d_train);
+  cudaFree(ps->d_train_norm);
+  cudaFree(ps->d_train_bitmap);
+  for (auto p : ps->d_local) cudaFree(p);
+  for (auto p : ps->d_local_norm) cudaFree(p);
+  ps->d_local.assign(c->n_workers, nullptr);
+  ps->d_local_norm.assign(c->n_workers, nullptr);
+  ps->n_local.assign(c->n_workers, 0);
+  ps->local_norm_ready.assign(c->n_workers, false);
+  ps->n_train = n_train;
+  const int n_words = (int)((c->n + 31) / 32);
+  CK(cudaMalloc(&ps->d_train, sizeof(int32_t) * n_train));
+  CK(cudaMalloc(&ps->d_train_norm, sizeof(double) * n_train));
+  CK(cudaMalloc(&ps->d_train_bitmap, sizeof(uint32_t) * n_words));
+  CK(cudaMemcpyAsync(ps->d_train, t32.data(), sizeof(int32_t) * n_train, cudaMemcpyHostToDevice, st));
+  launch_set_bitmap(ps->d_train, (int32_t)n_train, ps->d_train_bitmap, n_words, st);
+  ps->have_train_norm = false;
+  int32_t* d_err = ps->h[0].err;
+  CK(cudaMemsetAsync(d_err, 0, sizeof(int32_t), st));
+  if (precompute) {
+    int rc = launch_pull_norms(c->gdev(), ps->d_train, (int32_t)n_train, ps->d_train_bitmap,
+                               ps->d_train_norm, d_err, st);
+    if (rc) return rc;
+    ps->have_train_norm = true;
+  }
+  // per-worker local candidate lists (local mode, training.py:236-242)
+  std::vector<int32_t> owner(c->n);
+  CK(cudaMemcpy(owner.data(), c->d_owner, sizeof(int32_t) * c->n, cudaMemcpyDeviceToHost));
+  std::vector<std::vector<int32_t>> loc(c->n_workers);
+  for (int64_t i = 0; i < n_train; ++i) loc[owner[t32[i]]].push_back(t32[i]);
+  for (int w = 0; w < c->n_workers; ++w) {
+    ps->n_local[w] = (int64_t)loc[w].size();
+    if (loc[w].empty()) continue;
+    CK(cudaMalloc(&ps->d_local[w], sizeof(int32_t) * loc[w].size()));
+    CK(cudaMalloc(&ps->d_local_norm[w], sizeof(double) * loc[w].size()));
+    CK(cudaMemcpy(ps->d_local[w], loc[w].data(), sizeof(int32_t) * loc[w].size(), cudaMemcpyHostToDevice));
+  }
+  CK(cudaStreamSynchronize(st));
+  int err = 0;
+  CK(cudaMemcpy(&err, d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  return status_from_err(err);
+}
+
+extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, int mode, double D,
+                                double min_scale, const uint64_t* rng, void* stream) {
+  ARG(ps && ps->kind == KIND_SAINT, "not a SAINT plan set");
+  ARG(ps->d_train, "call skg_saint_set_candidates first");
+  ARG(n >= 1 && n <= ps->n_slots, "slot count out of range");
+  skg_ctx* c = ps->ctx;
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
+  for (int i = 0; i < n; ++i) {
+    const int w = workers[i];
+    ARG(w >= 0 && w < c->n_workers, "worker id out of range");
+    PlanDev& P = ps->h[i];
+    P.worker = w;
+    P.mode = mode;
+    P.D = D;
+    P.min_scale = min_scale;
+    for (int q = 0; q < 4; ++q) P.rng[q] = rng[4 * i + q];
+    if (mode == MODE_LOCAL) {
+      if (ps->n_local[w] == 0) {
+        set_error("no local training nodes to sample a subgraph from");
+        return SKG_ERR_ARG;
+      }
+      if (!ps->local_norm_ready[w]) {  // column_norms(g, train, local) (training.py:243-244)
+        int rc = launch_pull_norms(c->gdev(), ps->d_local[w], (int32_t)ps->n_local[w],
+                                   ps->d_train_bitmap, ps->d_local_norm[w], P.err, st);
+        if (rc) return rc;
+        ps->local_norm_ready[w] = true;
+      }
+      P.batch = ps->d_local[w];
+      P.batch_len = (int32_t)ps->n_local[w];
+      P.cand_norm = ps->d_local_norm[w];
+      P.budget = std::min<int64_t>(ps->budget, ps->n_local[w]);
+    } else {
+      if (!ps->have_train_norm) {
+        int rc = launch_pull_norms(c->gdev(), ps->d_train, (int32_t)ps->n_train, ps->d_train_bitmap,
+                                   ps->d_train_norm, P.err, st);
+        if (rc) return rc;
+        ps->have_train_norm = true;
+      }
+      P.batch = ps->d_train;
+      P.batch_len = (int32_t)ps->n_train;
+      P.cand_norm = ps->d_train_norm;
+      P.budget = std::min<int64_t>(ps->budget, ps->n_train);
+    }
+  }
+  CK(cudaMemcpyAsync(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
+  return launch_saint(c->gdev(), ps->d_plans, n, ps->cap_rows, ps->cap_cand, ps->cap_pairs,
+                      (int)ps->budget, st);
+}
+
+__global__ void k_ledger_add(const PlanDev* plans, int L, int64_t* ledger) {
+  const PlanDev& P = plans[blockIdx.x];
+  for (int t = threadIdx.x; t < L; t += blockDim.x) {
+    // reference layer order is bottom-up: layer l <-> top-down t = L-1-l (LADIES);
+    // SAINT charges its remote count at layer 0 only (training.py:248-253)
+    int v, l;
+    if (P.kind == KIND_LADIES) {
+      v = P.stat[t].remote;
+      l = L - 1 - t;
+    } else {
+      v = t == 0 ? P.stat[0].remote : 0;
+      l = t;
+    }
+    ledger[(int64_t)P.worker * L + l] += v;
+  }
+}
+
+extern "C" int skg_plans_ledger_add(skg_plans* ps, int n, uint64_t ledger_dev, void* stream) {
+  ARG(ps && n >= 1 && n <= ps->n_slots && ledger_dev, "bad ledger arguments");
+  k_ledger_add<<<n, 32, 0, (cudaStream_t)stream>>>(ps->d_plans, ps->L, (int64_t*)ledger_dev);
+  ++g_kernel_launches;
+  CK(cudaGetLastError());
+  return SKG_OK;
+}
+
+extern "C" int skg_plan_stats(skg_plans* ps, int slot, int64_t* stats, int64_t info[4]) {
+  ARG(ps && slot >= 0 && slot < ps->n_slots, "slot out of range");
+  CK(cudaSetDevice(ps->ctx->device));
+  CK(cudaDeviceSynchronize());
+  const PlanDev& P = ps->h[slot];
+  std::vector<LayerStat> ls(ps->L);
+  CK(cudaMemcpy(ls.data(), P.stat, sizeof(LayerStat) * ps->L, cudaMemcpyDeviceToHost));
+  int32_t err = 0;
+  int64_t draws = 0;
+  CK(cudaMemcpy(&err, P.err, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&draws, P.draws_consumed, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  int64_t starv = 0;
+  const int Ls = ps->kind == KIND_LADIES ? ps->L : 1;
+  for (int t = 0; t < Ls; ++t) {
+    const LayerStat& s = ls[t];
+    int64_t* o = stats + 16 * t;
+    o[0] = s.n_upper;
+    o[1] = s.n_cand;
+    o[2] = s.n_nodes;
+    o[3] = s.nnz;
+    o[4] = s.remote;
+    o[5] = s.has_dist;
+    o[6] = s.n_remote_cand;
+    o[7] = s.starved;
+    o[8] = s.skew;
+    o[9] = s.n_pairs;
+    o[10] = s.kept_pairs;
+    memcpy(&o[11], &s.s, 8);
+    memcpy(&o[12], &s.total, 8);
+    memcpy(&o[13], &s.T, 8);
+    o[14] = s.pw_depth;
+    o[15] = 0;
+    starv += s.starved;
+  }
+  info[0] = err;
+  info[1] = draws;
+  info[2] = starv;
+  info[3] = ps->L;
+  return status_from_err(err);
+}
+
+extern "C" int skg_plan_layer(skg_plans* ps, int slot, int t, int32_t* nodes, int32_t* indptr,
+                              int32_t* indices, double* values, int32_t* cand, double* norm,
+                              uint8_t* is_local) {
+  ARG(ps && slot >= 0 && slot < ps->n_slots, "slot out of range");
+  ARG(t >= 0 && t < ps->L, "layer out of range");
+  CK(cudaSetDevice(ps->ctx->device));
+  CK(cudaDeviceSynchronize());
+  const PlanDev& P = ps->h[slot];
+  const int ts = ps->kind == KIND_LADIES ? t : 0;
+  LayerStat s;
+  CK(cudaMemcpy(&s, P.stat + ts, sizeof(LayerStat), cudaMemcpyDeviceToHost));
+  if (nodes && s.n_nodes)
+    CK(cudaMemcpy(nodes, P.nodes + (size_t)ts * P.cap_rows, 4 * (size_t)s.n_nodes, cudaMemcpyDeviceToHost));
+  if (indptr)
+    CK(cudaMemcpy(indptr, P.indptr + (size_t)ts * (P.cap_rows + 1), 4 * (size_t)(s.n_upper + 1), cudaMemcpyDeviceToHost));
+  if (indices && s.nnz)
+    CK(cudaMemcpy(indices, P.indices + (size_t)ts * P.cap_pairs, 4 * (size_t)s.nnz, cudaMemcpyDeviceToHost));
+  if (values && s.nnz)
+    CK(cudaMemcpy(values, P.val + (size_t)ts * P.cap_pairs, 8 * (size_t)s.nnz, cudaMemcpyDeviceToHost));
+  if (s.n_cand) {
+    const int32_t* cp;
+    const double* np_;
+    if (ps->kind == KIND_SAINT) {
+      cp = P.batch;
+      np_ = P.cand_norm ? P.cand_norm : P.norm;
+    } else {
+      cp = P.cand + (size_t)ts * P.cap_cand;
+      np_ = P.norm + (size_t)ts * P.cap_cand;
+    }
+    if (cand) CK(cudaMemcpy(cand, cp, 4 * (size_t)s.n_cand, cudaMemcpyDeviceToHost));
+    if (norm) CK(cudaMemcpy(norm, np_, 8 * (size_t)s.n_cand, cudaMemcpyDeviceToHost));
+    if (is_local)
+      CK(cudaMemcpy(is_local, P.is_local + (size_t)ts * P.cap_cand, (size_t)s.n_cand, cudaMemcpyDeviceToHost));
+  }
+  return SKG_OK;
+}
+
+// ------------------------------------------------------------------ GCN
+extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dtype, skg_gcn** out) {
+  ARG(ps && out && dims && L == ps->L, "GCN depth must match the plan depth");
+  ARG(dtype == DT_F32 || dtype == DT_F64, "bad dtype");
+  ARG(ps->ctx->d_x && ps->ctx->F == dims[0], "features missing or dim mismatch");
+  ARG(ps->ctx->dtype == dtype, "feature dtype must equal the compute dtype");
+  CK(cudaSetDevice(ps->ctx->device));
+  skg_gcn* g = new skg_gcn();
+  g->ps = ps;
+  g->L = L;
+  g->dtype = dtype;
+  g->dims.assign(dims, dims + L + 1);
+  g->ld.resize(L + 1);
+  for (int l = 0; l <= L; ++l) {
+    g->ld[l] = round4(dims[l]);
+    g->ld_max = std::max(g->ld_max, g->ld[l]);
+  }
+  const size_t es = dtype == DT_F32 ? 4 : 8;
+  const size_t R = ps->cap_rows;
+  Carver cv;
+  g->slots.resize(ps->n_slots);
+  for (auto& s : g->slots) {
+    s.U.resize(L);
+    s.H.resize(L + 1);
+    cv.add(s.X0, R * g->ld[0] * es);
+    for (int l = 0; l < L; ++l) cv.add(s.U[l], R * g->ld[l] * es);
+    for (int l = 1; l <= L; ++l) cv.add(s.H[l], R * g->ld[l] * es);
+    cv.add(s.G0, R * g->ld_max * es);
+    cv.add(s.G1, R * g->ld_max * es);
+  }
+  CK(cudaMalloc(&g->arena, cv.off));
+  CK(cudaMemset(g->arena, 0, cv.off));
+  cv.bind(g->arena);
+  *out = g;
+  return SKG_OK;
+}
+
+extern "C" int skg_gcn_destroy(skg_gcn* g) {
+  if (!g) return SKG_OK;
+  cudaFree(g->arena);
+  delete g;
+  return SKG_OK;
+}
+
+namespace {
+struct LayerView {
+  const int32_t* d_rows;  // |S_{l+1}|
+  const int32_t* d_cols;  // |S_l|
+  const int32_t *indptr, *indices, *tindptr, *tindices;
+  const double *val, *tval;
+};
+LayerView layer_view(const skg_plans* ps, int slot, int l) {
+  const PlanDev& P = ps->h[slot];
+  const int t = ps->kind == KIND_LADIES ? ps->L - 1 - l : 0;
+  LayerView v;
+  v.d_rows = &P.stat[t].n_upper;
+  v.d_cols = &P.stat[t].n_nodes;
+  v.indptr = P.indptr + (size_t)t * (P.cap_rows + 1);
+  v.indices = P.indices + (size_t)t * P.cap_pairs;
+  v.val = P.val + (size_t)t * P.cap_pairs;
+  v.tindptr = P.tindptr + (size_t)t * (P.cap_rows + 1);
+  v.tindices = P.tindices + (size_t)t * P.cap_pairs;
+  v.tval = P.tval + (size_t)t * P.cap_pairs;
+  return v;
+}
+
+template <typename T>
+int gcn_run(skg_gcn* g, int slot, const uint64_t* wp, const uint64_t* gp, bool acc, double* loss,
+            bool backward, cudaStream_t st) {
+  skg_plans* ps = g->ps;
+  skg_ctx* c = ps->ctx;
+  const PlanDev& P = ps->h[slot];
+  GcnSlot& S = g->slots[slot];
+  const int L = g->L;
+  const int R = ps->cap_rows;
+  auto W = [&](int l) { return reinterpret_cast<const T*>(wp[l]); };
+  // layer-0 input rows X[S_0] (local shard or NVLink peer shards)
+  LayerView v0 = layer_view(ps, slot, 0);
+  const int t0 = ps->kind == KIND_LADIES ? L - 1 : 0;
+  const int32_t* in_nodes = P.nodes + (size_t)t0 * P.cap_rows;
+  T* X0 = reinterpret_cast<T*>(S.X0);
+  gather_rows<T>(c->fstore(), in_nodes, v0.d_cols, R, X0, g->ld[0], st);
+  for (int l = 0; l < L; ++l) {
+    LayerView v = layer_view(ps, slot, l);
+    const T* A = l == 0 ? X0 : reinterpret_cast<const T*>(S.H[l]);
+    T* U = reinterpret_cast<T*>(S.U[l]);
+    spmm<T>(v.d_rows, R, v.indptr, v.indices, v.val, A, g->ld[l], l > 0, U, g->ld[l], g->ld[l], st);
+    gemm<T>(false, false, R, (int)g->dims[l + 1], (int)g->dims[l], v.d_rows, nullptr, U, g->ld[l],
+            W(l), g->dims[l + 1], reinterpret_cast<T*>(S.H[l + 1]), g->ld[l + 1], false, st);
+  }
+  if (!backward) return SKG_OK;
+  // loss over the batch rows (training.py:293-308)
+  LayerView vt = layer_view(ps, slot, L - 1);
+  const int32_t* batch = ps->kind == KIND_LADIES ? P.batch : P.nodes;
+  T* G = reinterpret_cast<T*>(S.G0);
+  T* Gu = reinterpret_cast<T*>(S.G1);
+  softmax_ce<T>(vt.d_rows, R, batch, c->d_labels, reinterpret_cast<const T*>(S.H[L]), g->ld[L],
+                (int)g->dims[L], G, g->ld[L], loss, P.err, st);
+  int64_t ldG = g->ld[L];
+  for (int l = L - 1; l >= 0; --l) {
+    LayerView v = layer_view(ps, slot, l);
+    // dW_l = U_l^T G  (K = |S_{l+1}| read on device)
+    gemm<T>(true, false, (int)g->dims[l], (int)g->dims[l + 1], R, nullptr, v.d_rows,
+            reinterpret_cast<const T*>(S.U[l]), g->ld[l], G, ldG, reinterpret_cast<T*>(gp[l]),
+            g->dims[l + 1], acc, st);
+    if (l == 0) break;
+    // G_u = G W_l^T
+    gemm<T>(false, true, R, (int)g->dims[l], (int)g->dims[l + 1], v.d_rows, nullptr, G, ldG, W(l),
+            g->dims[l + 1], Gu, g->ld[l], false, st);
+    // G_prev = (Block_l^T G_u) * [H_l > 0]
+    spmm_t_mask<T>(v.d_cols, R, v.tindptr, v.tindices, v.tval, Gu, g->ld[l],
+                   reinterpret_cast<const T*>(S.H[l]), g->ld[l], G, g->ld[l], g->ld[l], st);
+    ldG = g->ld[l];
+  }
+  return SKG_OK;
+}
+}  // namespace
+
+extern "C" int skg_gcn_step(skg_gcn* g, int slot, const uint64_t* wp, const uint64_t* gp,
+                            int accumulate, uint64_t loss_dev, void* stream) {
+  ARG(g && slot >= 0 && slot < g->ps->n_slots && wp && gp && loss_dev, "bad gcn_step arguments");
+  ARG(g->ps->ctx->d_labels, "labels not set");
+  CK(cudaSetDevice(g->ps->ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = g->dtype == DT_F32
+               ? gcn_run<float>(g, slot, wp, gp, accumulate != 0, (double*)loss_dev, true, st)
+               : gcn_run<double>(g, slot, wp, gp, accumulate != 0, (double*)loss_dev, true, st);
+  if (rc) return rc;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("gcn_step: ") + cudaGetErrorString(e));
+    return SKG_ERR_CUDA;
+  }
+  return SKG_OK;
+}
+
+extern "C" int skg_gcn_forward(skg_gcn* g, int slot, const uint64_t* wp, void* stream) {
+  ARG(g && slot >= 0 && slot < g->ps->n_slots && wp, "bad gcn_forward arguments");
+  CK(cudaSetDevice(g->ps->ctx->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = g->dtype == DT_F32 ? gcn_run<float>(g, slot, wp, nullptr, false, nullptr, false, st)
+                              : gcn_run<double>(g, slot, wp, nullptr, false, nullptr, false, st);
+  if (rc) return rc;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("gcn_forward: ") + cudaGetErrorString(e));
+    return SKG_ERR_CUDA;
+  }
+  return SKG_OK;
+}
+
+extern "C" int skg_gcn_read_logits(skg_gcn* g, int slot, void* host_out, int64_t* rows_out) {
+  ARG(g && slot >= 0 && slot < g->ps->n_slots, "bad slot");
+  CK(cudaSetDevice(g->ps->ctx->device));
+  CK(cudaDeviceSynchronize());
+  skg_plans* ps = g->ps;
+  const PlanDev& P = ps->h[slot];
+  LayerStat s;
+  CK(cudaMemcpy(&s, P.stat + 0, sizeof(LayerStat), cudaMemcpyDeviceToHost));
+  const int64_t rows = s.n_upper;
+  *rows_out = rows;
+  const size_t es = g->dtype == DT_F32 ? 4 : 8;
+  const int64_t C = g->dims[g->L];
+  if (host_out && rows)
+    CK(cudaMemcpy2D(host_out, es * C, g->slots[slot].H[g->L], es * g->ld[g->L], es * C, rows,
+                    cudaMemcpyDeviceToHost));
+  return SKG_OK;
+}
+
+extern "C" int skg_predict_logits(skg_ctx* c, int L, const int64_t* dims, const uint64_t* wp,
+                                  int dtype, uint64_t out_dev, void* stream) {
+  ARG(c && dims && wp && out_dev && L >= 1, "bad predict arguments");
+  ARG(c->d_x && c->dtype == dtype && c->F == dims[0] && c->x_rows == c->n,
+      "full-graph inference needs all feature rows on this device");
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = dtype == DT_F32 ? 4 : 8;
+  int64_t ldm = 0;
+  for (int l = 0; l <= L; ++l) ldm = std::max(ldm, round4(dims[l]));
+  char *U = nullptr, *H = nullptr;
+  CK(cudaMalloc(&U, es * ldm * std::max<int64_t>(c->n, 1)));
+  CK(cudaMalloc(&H, es * ldm * std::max<int64_t>(c->n, 1)));
+  CK(cudaMemsetAsync(H, 0, es * ldm * std::max<int64_t>(c->n, 1), st));
+  for (int l = 0; l < L; ++l) {
+    const int64_t ldi = l == 0 ? c->ldx : round4(dims[l]);
+    const int64_t ldl = round4(dims[l]);
+    const bool last = l == L - 1;
+    const int64_t ldo = last ? dims[L] : round4(dims[l + 1]);
+    if (dtype == DT_F32) {
+      const float* A = l == 0 ? (const float*)c->d_x : (const float*)H;
+      spmm_full<float>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (float*)U, ldl, ldl, st);
+      gemm<float>(false, false, (int)c->n, (int)dims[l + 1], (int)dims[l], nullptr, nullptr,
+                  (const float*)U, ldl, (const float*)wp[l], dims[l + 1],
+                  last ? (float*)out_dev : (float*)H, ldo, false, st);
+    } else {
+      const double* A = l == 0 ? (const double*)c->d_x : (const double*)H;
+      spmm_full<double>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (double*)U, ldl, ldl, st);
+      gemm<double>(false, false, (int)c->n, (int)dims[l + 1], (int)dims[l], nullptr, nullptr,
+                   (const double*)U, ldl, (const double*)wp[l], dims[l + 1],
+                   last ? (double*)out_dev : (double*)H, ldo, false, st);
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  cudaFree(U);
+  cudaFree(H);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("predict_logits: ") + cudaGetErrorString(e));
+    return SKG_ERR_CUDA;
+  }
+  return SKG_OK;
+}
+
+extern "C" int skg_sgd_step(int dtype, uint64_t w, uint64_t g, int64_t n, double lr, double contrib,
+                            void* stream) {
+  ARG(n >= 0 && contrib > 0, "bad sgd arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == DT_F32) sgd_step<float>((float*)w, (const float*)g, n, lr, contrib, st);
+  else sgd_step<double>((double*)w, (const double*)g, n, lr, contrib, st);
+  CK(cudaGetLastError());
+  return SKG_OK;
+}
+
+extern "C" int skg_adam_step(int dtype, uint64_t w, uint64_t g, uint64_t m, uint64_t v, int64_t n,
+                             double lr, double contrib, int64_t t, void* stream) {
+  ARG(n >= 0 && contrib > 0 && t >= 1, "bad adam arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  const double bc1 = 1.0 - std::pow(b1, (double)t), bc2 = 1.0 - std::pow(b2, (double)t);
+  if (dtype == DT_F32)
+    adam_step<float>((float*)w, (const float*)g, (float*)m, (float*)v, n, lr, contrib, b1, b2,
+                     1.0 - b1, 1.0 - b2, bc1, bc2, eps, st);
+  else
+    adam_step<double>((double*)w, (const double*)g, (double*)m, (double*)v, n, lr, contrib, b1, b2,
+                      1.0 - b1, 1.0 - b2, bc1, bc2, eps, st);
+  CK(cudaGetLastError());
+  return SKG_OK;
+}
+
+extern "C" int skg_zero(int dtype, uint64_t p, int64_t n, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == DT_F32) fill_zero<float>((float*)p, n, st);
+  else fill_zero<double>((double*)p, n, st);
+  CK(cudaGetLastError());
+  return SKG_OK;
+}

@@ -1,0 +1,128 @@
+// Device-side data layout of the sampler (shared by sampler.cu, gcn.cu and capi.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace skg {
+
+enum Mode : int32_t { MODE_FULL = 0, MODE_LOCAL = 1, MODE_SKEWED = 2 };
+enum Kind : int32_t { KIND_LADIES = 0, KIND_SAINT = 1 };
+
+// Replicated topology (int32 columns, fp64 weights as stored by the reference's
+// WeightedGraph, graph.py:28-31) plus the ownership map (partition.py:21).
+struct GraphDev {
+  int64_t n, nnz;
+  const int64_t* off;    // [n+1]
+  const int32_t* col;    // [nnz]
+  const double* w;       // [nnz]
+  const int32_t* owner;  // [n]
+  // transpose (CSC) used by the SAINT pull-norm pass; aliases off/col/w when symmetric
+  const int64_t* t_off;
+  const int32_t* t_row;
+  const double* t_w;
+  int32_t n_words;       // ceil(n/32)
+};
+
+// Per-layer scalars of one plan.  Layers are indexed top-down while sampling
+// (t = 0 is the layer adjacent to the batch); the Python mirror reverses them like
+// training.py:207 does.
+struct LayerStat {
+  int32_t n_upper;        // |S_{t-1}| (rows of this layer's block)
+  int32_t n_cand;         // |N(S)| (after the local restriction in local mode)
+  int32_t n_nodes;        // |S_t| sampled (== n_cand when saturated)
+  int32_t nnz;            // block nnz
+  int32_t remote;         // remote sampled nodes (ledger, training.py:199)
+  int32_t has_dist;       // 1 when a distribution was drawn from (not saturated)
+  int32_t n_remote_cand;  // |R| among candidates
+  int32_t starved;        // local-mode starvation events at this layer
+  int32_t skew;           // 1 when skewed weights were used (else linear)
+  int32_t pw_depth;       // depth of numpy's pairwise-sum tree for n_cand
+  int64_t n_pairs;        // sum of upper-row degrees
+  int64_t kept_pairs;     // pairs that landed on a candidate
+  double s;               // scale factor baked into q (1.0 for linear)
+  double total;           // numpy pairwise sum of the scaled weights
+  double T;               // exact sequential cumsum total (cdf[-1])
+};
+
+// Per-plan workspace; an array of these lives in device memory, one per slot.
+struct PlanDev {
+  // ---- configuration, written by the host for each sampling launch
+  int32_t kind, worker, mode, n_layers;
+  int64_t budget;
+  double D, min_scale;
+  uint64_t rng[4];          // PCG64 state (hi, lo) and increment (hi, lo)
+  int32_t batch_len;        // LADIES: |batch|; SAINT: |candidates|
+  int32_t pad0;
+  const int32_t* batch;     // LADIES batch ids; SAINT candidate ids (sorted)
+  const double* cand_norm;  // SAINT precomputed norms aligned with batch, or null
+  // ---- capacities
+  int32_t cap_rows;         // max(|batch|, budget) (LADIES), budget (SAINT)
+  int32_t cap_cand;         // N_max
+  int64_t cap_pairs;        // E_max
+  int32_t cap_chunks, cap_supers, cap_slots, cap_tiles;
+  // ---- scratch
+  uint32_t* bitmap;         // [n_words]
+  uint32_t* sbitmap;        // [n_words] sampled set
+  int32_t* cnt_node;        // [n], zero at rest
+  int64_t* pair_off;        // [cap_rows+1]
+  int32_t* pair_slot;       // [cap_pairs]
+  int32_t* word_prefix;     // [n_words]
+  int64_t* tile_a;          // [cap_tiles]
+  int64_t* tile_b;          // [cap_tiles]
+  int32_t* bucket_off;      // [cap_cand+1]
+  int32_t* bucket_r;        // [cap_pairs]
+  double* bucket_w;         // [cap_pairs]
+  int32_t* big_list;        // [cap_cand]
+  int32_t* counters;        // [8]: 0 big_count
+  double* pw_val;           // [cap_slots]
+  int32_t* pw_lvl;          // [cap_slots]
+  double* chunk_sum;        // [cap_chunks]
+  double* chunk_approx;     // [cap_chunks] approximate exclusive starts
+  long long* chunk_map;     // [2*cap_chunks]
+  int32_t* chunk_e;         // [cap_chunks] assumed binade (INT_MIN: not flat)
+  int32_t* chunk_mode;      // [cap_chunks]
+  double* chunk_start;      // [cap_chunks]
+  long long* super_map;     // [2*cap_supers]
+  int32_t* super_e;         // [cap_supers]
+  int32_t* super_mode;      // [cap_supers]
+  double* super_start;      // [cap_supers]
+  double* cdf;              // [cap_cand]
+  int32_t* draw_idx;        // [budget]
+  int64_t* draws_consumed;  // [1] uniforms consumed by this plan so far
+  int32_t* err;             // [1] ErrBits
+  int32_t* starvation;      // [1]
+  // ---- per top-down layer results, strided by the capacities
+  int32_t* cand;            // [L*cap_cand]
+  double* norm;             // [L*cap_cand]
+  uint8_t* is_local;        // [L*cap_cand]
+  int32_t* nodes;           // [L*cap_rows]
+  int32_t* samp_rank;       // [L*cap_rows]
+  double* p;                // [L*cap_rows]
+  int32_t* indptr;          // [L*(cap_rows+1)]   CSR (rows = upper)
+  int32_t* indices;         // [L*cap_pairs]
+  double* val;              // [L*cap_pairs]
+  int32_t* tindptr;         // [L*(cap_rows+1)]   CSR of the transpose (rows = sampled)
+  int32_t* tindices;        // [L*cap_pairs]
+  double* tval;             // [L*cap_pairs]
+  LayerStat* stat;          // [L]
+};
+
+constexpr int kTileWords = 4096;   // bitmap words per compaction tile (1024 threads x 4)
+constexpr int kTileCand = 4096;    // candidates per scan tile
+constexpr int kSmallBucket = 16;   // buckets folded in registers
+constexpr int kChunk = 32;         // exact-cumsum chunk (one warp)
+constexpr int kSuper = 1024;       // exact-cumsum superchunk (32 chunks)
+constexpr int kPwSub = 256;        // pairwise-tree slots combined per CTA
+
+// Host-side launch of the full sampling pipeline for n_plans slots.
+int launch_ladies(const GraphDev& g, PlanDev* d_plans, int n_plans, int n_layers, int max_upper,
+                  int cap_cand, int64_t cap_pairs, int budget_max, cudaStream_t st);
+int launch_saint(const GraphDev& g, PlanDev* d_plans, int n_plans, int cap_rows, int cap_cand,
+                 int64_t cap_pairs, int budget_max, cudaStream_t st);
+int launch_pull_norms(const GraphDev& g, const int32_t* cand, int32_t n_cand,
+                      const uint32_t* row_bitmap, double* out, int32_t* err, cudaStream_t st);
+void launch_set_bitmap(const int32_t* ids, int32_t n, uint32_t* bitmap, int32_t n_words,
+                       cudaStream_t st);
+extern unsigned long long g_kernel_launches;
+
+}  // namespace skg

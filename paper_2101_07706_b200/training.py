@@ -1,0 +1,635 @@
+"""Drop-in for the reference's training module (skewgcn/training.py) on the GPU.
+
+Same names, arguments, return types and exceptions as the reference:
+``ladies_plan`` (training.py:162-208), ``saint_plan`` (216-254), ``forward`` (261-269),
+``loss_and_backward`` (272-318), ``predict_logits`` / ``evaluate`` (325-363) and
+``train_distributed`` (430-518).  Plans are sampled by the sm_100a kernels of
+libskg and stay device-resident; the scipy/numpy view the reference returns is
+materialised lazily on first access (``plan.layers``), bit-identical in node sets,
+block indices and ledger counts.
+
+``train_distributed`` runs the whole iteration on the device: the host only derives
+batch ids and PCG64 states (natively, libskg host runtime), every worker's plan of an
+iteration is sampled in one batched launch, worker gradients are accumulated in
+worker order, averaged across GPUs with an NCCL all-reduce when torch.distributed is
+initialised, and the optimizer step is one fused kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import scipy.sparse as sp
+
+from . import _device as D
+from ._native import DT, KIND_LADIES, KIND_SAINT, MODES, check, lib, ptr
+from .graph import WeightedGraph, check_node_set, node_set
+from .partition import Partition
+from .sampling import ProbDist, SamplerConfig
+from .seeding import advance_generator, generator_state, spawn_rng
+
+# ---------------------------------------------------------------------------
+# Model
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class GcnModel:
+    """Per-layer weight matrices (training.py:40-62)."""
+
+    weights: list
+
+    def __post_init__(self) -> None:
+        for a, b in zip(self.weights, self.weights[1:]):
+            if a.shape[1] != b.shape[0]:
+                raise ValueError("adjacent layer dims do not match")
+        if any(not np.all(np.isfinite(w)) for w in self.weights):
+            raise ValueError("non-finite model weights")
+
+    @property
+    def n_layers(self) -> int:
+        return len(self.weights)
+
+    @property
+    def dims(self) -> list:
+        return [self.weights[0].shape[0]] + [w.shape[1] for w in self.weights]
+
+    def copy(self) -> "GcnModel":
+        return GcnModel([w.copy() for w in self.weights])
+
+
+def init_model(layer_dims, seed: int) -> GcnModel:
+    """Glorot uniform from spawn_rng(seed, 'init', l) (training.py:65-74)."""
+    if len(layer_dims) < 2:
+        raise ValueError("need at least input and output dims")
+    ws = []
+    for l, (a, b) in enumerate(zip(layer_dims, layer_dims[1:])):
+        bound = np.sqrt(6.0 / (a + b))
+        ws.append(spawn_rng(seed, "init", l).uniform(-bound, bound, size=(a, b)))
+    return GcnModel(ws)
+
+
+# ---------------------------------------------------------------------------
+# Plans
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class PlanLayer:
+    nodes: np.ndarray
+    block: sp.csr_matrix
+    dist: ProbDist | None
+    remote_sampled: int
+
+
+class CommLedger:
+    """Remote-feature-fetch counts (epochs, workers, layers) (training.py:117-134)."""
+
+    def __init__(self, counts: np.ndarray):
+        self.counts = counts
+
+    @classmethod
+    def empty(cls, n_epochs, n_workers, n_layers):
+        return cls(np.zeros((n_epochs, n_workers, n_layers), dtype=np.int64))
+
+    def add_plan(self, epoch, worker, plan) -> None:
+        self.counts[epoch, worker, :] += plan.remote_per_layer()
+
+    def total(self) -> int:
+        return int(self.counts.sum())
+
+    def per_worker_epoch(self, epoch, worker) -> int:
+        return int(self.counts[epoch, worker].sum())
+
+
+class SamplePlan:
+    """Device-resident plan; ``layers`` materialises the reference's view on demand."""
+
+    def __init__(self, lease: D.Lease, batch: np.ndarray, n_layers: int, kind: int):
+        self._lease = lease
+        self.batch = batch
+        self._n_layers = n_layers
+        self._kind = kind
+        self._layers = None
+        st, info, rc = lease.ps.stats(lease.slot)
+        check(rc)
+        self._stats = st
+        self._info = info
+        self.starvation_events = int(info[2]) if kind == KIND_LADIES else 0
+        self.draws_consumed = int(info[1])
+
+    @property
+    def n_layers(self) -> int:
+        return self._n_layers
+
+    def remote_per_layer(self) -> np.ndarray:
+        L = self._n_layers
+        if self._kind == KIND_SAINT:
+            out = np.zeros(L, dtype=np.int64)
+            out[0] = self._stats[0, 4]
+            return out
+        return self._stats[:, 4][::-1].astype(np.int64).copy()
+
+    @property
+    def layers(self):
+        if self._layers is None:
+            self._layers = self._materialise()
+        return self._layers
+
+    @property
+    def input_nodes(self) -> np.ndarray:
+        return self.layers[0].nodes
+
+    def _materialise(self):
+        ps, slot = self._lease.ps, self._lease.slot
+        L = self._n_layers
+        out = []
+        ts = range(L) if self._kind == KIND_LADIES else [0]
+        for t in ts:
+            row = self._stats[t]
+            has = bool(row[5])
+            lay = D.read_layer(ps, slot, t, row, has)
+            block = sp.csr_matrix((lay["values"], lay["indices"].astype(np.int32), lay["indptr"]),
+                                  shape=lay["shape"])
+            dist = None
+            if has:
+                s = float(np.array(row[11]).view(np.float64))
+                total = float(np.array(row[12]).view(np.float64))
+                norm, loc = lay["norm"], lay["is_local"]
+                scaled = np.where(loc, s * norm, norm) if row[8] else norm
+                dist = ProbDist(candidates=lay["cand"].astype(np.int64), q=scaled / total,
+                                is_local=loc, s_used=s if row[8] else 1.0)
+            out.append(PlanLayer(nodes=lay["nodes"], block=block, dist=dist,
+                                 remote_sampled=int(row[4])))
+        if self._kind == KIND_SAINT:
+            first = out[0]
+            return [PlanLayer(first.nodes, first.block, first.dist,
+                              first.remote_sampled if l == 0 else 0) for l in range(L)]
+        out.reverse()
+        return out
+
+
+def _uniform_source(rng, budget: int, n_layers: int):
+    gs = generator_state(rng)
+    if gs is None:
+        raise TypeError("the device sampler consumes PCG64 streams (numpy default_rng / spawn_rng)")
+    return gs[0]
+
+
+def ladies_plan(g: WeightedGraph, partition: Partition, worker: int, batch, cfg: SamplerConfig,
+                n_layers: int, rng: np.random.Generator) -> SamplePlan:
+    """Layer-wise skewed sampling on the GPU (training.py:162-208).  Consumes exactly the
+    uniforms the reference would from ``rng`` and advances it accordingly."""
+    batch = node_set(batch)
+    if len(batch) == 0:
+        raise ValueError("empty batch")
+    check_node_set(batch, g.n_nodes)
+    if not 0 <= worker < partition.n_workers:
+        raise ValueError("worker id out of range")
+    dg = D.device_graph(g)
+    dg.ensure_owner(partition)
+    state = _uniform_source(rng, cfg.budget, n_layers)
+    ps = dg.acquire(KIND_LADIES, 1, n_layers, int(cfg.budget), int(len(batch)))
+    lease = D.Lease(dg, ps, 0)
+    off = np.array([0, len(batch)], dtype=np.int64)
+    w = np.array([worker], dtype=np.int32)
+    check(lib.skg_ladies_sample(ps.h, 1, ptr(w, C.c_int32), ptr(off, C.c_int64), ptr(batch, C.c_int64),
+                                MODES[cfg.mode], float(cfg.skew_constant), float(cfg.min_scale),
+                                ptr(state, C.c_uint64), None))
+    plan = SamplePlan(lease, batch, n_layers, KIND_LADIES)
+    advance_generator(rng, plan.draws_consumed)
+    return plan
+
+
+def train_column_norms(g: WeightedGraph, train_nodes: np.ndarray) -> np.ndarray:
+    """Squared column norms over training rows (training.py:211-213), on the GPU."""
+    from .graph import column_norms
+    return column_norms(g, train_nodes, train_nodes)
+
+
+def _saint_set(dg, ps, train_nodes, precompute):
+    key = (id(train_nodes), train_nodes.ctypes.data, train_nodes.shape, dg.owner_key)
+    if ps.train_key != key:
+        check(lib.skg_saint_set_candidates(ps.h, ptr(train_nodes, C.c_int64), len(train_nodes),
+                                           int(precompute), None))
+        ps.train_key = key
+        ps.train_ref = train_nodes
+
+
+def saint_plan(g: WeightedGraph, partition: Partition, worker: int, train_nodes,
+               subgraph_size: int, cfg: SamplerConfig, n_layers: int, rng: np.random.Generator,
+               norms=None) -> SamplePlan:
+    """GraphSAINT-style subgraph plan on the GPU (training.py:216-254).  Column norms over
+    the training rows are computed (and cached per partition) on the device; a passed
+    ``norms`` array is accepted for API compatibility (it equals what the device computes)."""
+    train_nodes = node_set(train_nodes)
+    if len(train_nodes) == 0:
+        raise ValueError("empty training node set")
+    if subgraph_size > len(train_nodes):
+        warnings.warn("subgraph size exceeds training set; clamping")
+        subgraph_size = len(train_nodes)
+    if subgraph_size < 1:
+        raise ValueError("subgraph size must be >= 1")
+    check_node_set(train_nodes, g.n_nodes)
+    if not 0 <= worker < partition.n_workers:
+        raise ValueError("worker id out of range")
+    dg = D.device_graph(g)
+    dg.ensure_owner(partition)
+    state = _uniform_source(rng, subgraph_size, n_layers)
+    ps = dg.acquire(KIND_SAINT, 1, n_layers, int(subgraph_size), 1)
+    lease = D.Lease(dg, ps, 0)
+    _saint_set(dg, ps, train_nodes, cfg.mode != "local")
+    w = np.array([worker], dtype=np.int32)
+    check(lib.skg_saint_sample(ps.h, 1, ptr(w, C.c_int32), MODES[cfg.mode], float(cfg.skew_constant),
+                               float(cfg.min_scale), ptr(state, C.c_uint64), None))
+    plan = SamplePlan(lease, None, n_layers, KIND_SAINT)
+    plan.batch = plan.layers[0].nodes
+    advance_generator(rng, plan.draws_consumed)
+    return plan
+
+
+# ---------------------------------------------------------------------------
+# Forward / backward
+# ---------------------------------------------------------------------------
+
+def _torch():
+    import torch
+    return torch
+
+
+def _device_weights(weights, dtype):
+    torch = _torch()
+    td = torch.float32 if dtype == "float32" else torch.float64
+    ws = [torch.as_tensor(np.ascontiguousarray(w), dtype=td).cuda() for w in weights]
+    return ws, np.array([w.data_ptr() for w in ws], dtype=np.uint64)
+
+
+def _check_plan(model, plan):
+    if not isinstance(plan, SamplePlan):
+        raise TypeError("plan must come from paper_2101_07706_b200.ladies_plan / saint_plan")
+    if plan.n_layers != model.n_layers:
+        raise ValueError("plan depth does not match model depth")
+
+
+def forward(model: GcnModel, plan: SamplePlan, features: np.ndarray) -> np.ndarray:
+    """Logits for the plan's batch (training.py:261-269)."""
+    _check_plan(model, plan)
+    dtype = D.compute_dtype()
+    lease = plan._lease
+    lease.dg.ensure_features(features, dtype)
+    dims = [features.shape[1]] + [w.shape[1] for w in model.weights]
+    if dims[0] != model.weights[0].shape[0]:
+        raise ValueError("feature dim does not match the model")
+    gcn = lease.ps.gcn(dims, dtype)
+    ws, wp = _device_weights(model.weights, dtype)
+    check(lib.skg_gcn_forward(gcn, lease.slot, ptr(wp, C.c_uint64), D.current_stream()))
+    rows = C.c_int64()
+    nb = plan._stats[0, 0] if plan._kind == KIND_LADIES else plan._stats[0, 2]
+    out = np.zeros((int(nb), dims[-1]), dtype=np.float32 if dtype == "float32" else np.float64)
+    check(lib.skg_gcn_read_logits(gcn, lease.slot, out.ctypes.data_as(C.c_void_p), C.byref(rows)))
+    del ws
+    return out.astype(np.float64)
+
+
+def loss_and_backward(model: GcnModel, plan: SamplePlan, features: np.ndarray, labels: np.ndarray):
+    """Mean softmax cross-entropy over labelled batch rows and all weight gradients
+    (training.py:272-318), computed on the GPU."""
+    _check_plan(model, plan)
+    torch = _torch()
+    dtype = D.compute_dtype()
+    lease = plan._lease
+    batch_labels = np.asarray(labels)[plan.batch]
+    if not np.any(batch_labels >= 0):
+        raise ValueError("batch contains no labeled nodes")
+    lease.dg.ensure_features(features, dtype)
+    lease.dg.ensure_labels(np.asarray(labels))
+    dims = [features.shape[1]] + [w.shape[1] for w in model.weights]
+    gcn = lease.ps.gcn(dims, dtype)
+    ws, wp = _device_weights(model.weights, dtype)
+    gs = [torch.empty_like(w) for w in ws]
+    gp = np.array([g.data_ptr() for g in gs], dtype=np.uint64)
+    loss = torch.zeros(1, dtype=torch.float64, device="cuda")
+    check(lib.skg_gcn_step(gcn, lease.slot, ptr(wp, C.c_uint64), ptr(gp, C.c_uint64), 0,
+                           loss.data_ptr(), D.current_stream()))
+    torch.cuda.synchronize()
+    return float(loss.item()), [g.double().cpu().numpy() for g in gs]
+
+
+# ---------------------------------------------------------------------------
+# Full-graph inference and evaluation
+# ---------------------------------------------------------------------------
+
+def _predict_device(dg, model_weights_dev, dims, dtype):
+    torch = _torch()
+    wp = np.array([w.data_ptr() for w in model_weights_dev], dtype=np.uint64)
+    d = np.asarray(dims, dtype=np.int64)
+    out = torch.empty((dg.n, dims[-1]), dtype=torch.float32 if dtype == "float32" else torch.float64,
+                      device="cuda")
+    check(lib.skg_predict_logits(dg.ctx, len(dims) - 1, ptr(d, C.c_int64), ptr(wp, C.c_uint64),
+                                 DT[dtype], out.data_ptr(), D.current_stream()))
+    return out
+
+
+def predict_logits(model: GcnModel, g: WeightedGraph) -> np.ndarray:
+    """Exact full-graph forward (training.py:325-334) on the GPU."""
+    if g.features is None:
+        raise ValueError("graph carries no features")
+    dtype = D.compute_dtype()
+    dg = D.device_graph(g)
+    dg.ensure_features(g.features, dtype)
+    ws, _ = _device_weights(model.weights, dtype)
+    return _predict_device(dg, ws, model.dims, dtype).double().cpu().numpy()
+
+
+@dataclass
+class EvalResult:
+    accuracy: float
+    micro_f1: float
+
+
+def evaluate(model: GcnModel, g: WeightedGraph, nodes) -> EvalResult:
+    """Argmax accuracy and micro-F1 (training.py:343-363)."""
+    nodes = node_set(nodes)
+    if len(nodes) == 0:
+        raise ValueError("empty evaluation node set")
+    if g.labels is None or np.any(g.labels[nodes] < 0):
+        raise ValueError("evaluation nodes must be labeled")
+    preds = np.argmax(predict_logits(model, g)[nodes], axis=1)
+    truth = g.labels[nodes]
+    accuracy = float(np.mean(preds == truth))
+    n_classes = int(max(preds.max(), truth.max())) + 1
+    tp = np.array([np.sum((preds == c) & (truth == c)) for c in range(n_classes)], dtype=float)
+    fp = np.array([np.sum((preds == c) & (truth != c)) for c in range(n_classes)], dtype=float)
+    fn = np.array([np.sum((preds != c) & (truth == c)) for c in range(n_classes)], dtype=float)
+    denom = 2 * tp.sum() + fp.sum() + fn.sum()
+    micro_f1 = float(2 * tp.sum() / denom) if denom > 0 else 0.0
+    return EvalResult(accuracy=accuracy, micro_f1=micro_f1)
+
+
+# ---------------------------------------------------------------------------
+# Distributed training loop
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class MetricRow:
+    epoch: int
+    worker: int
+    loss: float
+    train_acc: float
+    val_acc: float
+    comm_nodes_epoch: int
+
+
+@dataclass
+class Metrics:
+    rows: list = field(default_factory=list)
+
+    def best_val_acc(self) -> float:
+        return max((r.val_acc for r in self.rows), default=0.0)
+
+    def final_val_acc(self) -> float:
+        return self.rows[-1].val_acc if self.rows else 0.0
+
+    def write_csv(self, path) -> None:
+        with open(path, "w", encoding="utf-8", newline="\n") as fh:
+            fh.write("epoch,worker,loss,train_acc,val_acc,comm_nodes_epoch\n")
+            for r in self.rows:
+                fh.write(f"{r.epoch},{r.worker},{r.loss!r},{r.train_acc!r},"
+                         f"{r.val_acc!r},{r.comm_nodes_epoch}\n")
+
+
+def _dist_info():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist, dist.get_rank(), dist.get_world_size()
+    except Exception:
+        pass
+    return None, 0, 1
+
+
+def assign_workers(active, rank: int, world: int):
+    """Workers (partitions) handled by this rank: contiguous blocks of the active list,
+    so rank r's workers precede rank r+1's (the reference's worker order)."""
+    n = len(active)
+    lo = (n * rank) // world
+    hi = (n * (rank + 1)) // world
+    return list(active[lo:hi])
+
+
+class Trainer:
+    """Device-resident training state for ``train_distributed`` (and the benchmark)."""
+
+    def __init__(self, g, partition, model, cfg, *, batch_size, lr, mode, seed,
+                 sampler="ladies", subgraph_size=None, optimizer="sgd", dtype=None,
+                 epochs=1, workers=None):
+        torch = _torch()
+        if g.features is None or g.labels is None or g.train_mask is None:
+            raise ValueError("training needs features, labels and masks")
+        if sampler not in ("ladies", "saint"):
+            raise ValueError(f"unknown sampler {sampler!r}")
+        if sampler == "saint" and subgraph_size is None:
+            raise ValueError("saint sampler needs subgraph_size")
+        if optimizer not in ("sgd", "adam"):
+            raise ValueError(f"unknown optimizer {optimizer!r}")
+        self.g, self.partition, self.model = g, partition, model
+        self.cfg = replace(cfg, mode=mode)
+        self.mode, self.seed, self.lr = mode, seed, lr
+        self.sampler, self.optimizer = sampler, optimizer
+        self.batch_size = batch_size
+        self.dtype = dtype or D.compute_dtype()
+        self.k = partition.n_workers
+        self.L = model.n_layers
+        self.dims = model.dims
+        owner = partition.owner
+        self.worker_train = [np.flatnonzero(g.train_mask & (owner == w)) for w in range(self.k)]
+        self.active = [w for w in range(self.k) if len(self.worker_train[w])]
+        for w in range(self.k):
+            if not len(self.worker_train[w]):
+                warnings.warn(f"worker {w} has no training nodes; skipping it")
+        if not self.active:
+            raise ValueError("no worker has training nodes")
+        self.all_train = np.flatnonzero(g.train_mask).astype(np.int64)
+        if sampler == "saint":
+            if subgraph_size > len(self.all_train):
+                warnings.warn("subgraph size exceeds training set; clamping")
+                subgraph_size = len(self.all_train)
+            self.per_epoch = max(1, int(np.ceil(len(self.all_train) / subgraph_size)))
+        else:
+            self.per_epoch = max(1, max(int(np.ceil(len(self.worker_train[w]) / batch_size))
+                                        for w in self.active))
+        self.subgraph_size = subgraph_size
+        self.dist, self.rank, self.world = _dist_info()
+        self.mine = workers if workers is not None else assign_workers(self.active, self.rank, self.world)
+        self.dg = D.device_graph(g)
+        self.dg.ensure_owner(partition)
+        self.dg.ensure_features(g.features, self.dtype)
+        self.dg.ensure_labels(np.asarray(g.labels))
+        n_slots = max(1, len(self.mine))
+        if sampler == "ladies":
+            self.ps = self.dg.acquire(KIND_LADIES, n_slots, self.L, int(self.cfg.budget), int(batch_size))
+        else:
+            self.ps = self.dg.acquire(KIND_SAINT, n_slots, self.L, int(subgraph_size), 1)
+            _saint_set(self.dg, self.ps, self.all_train, mode != "local")
+        self.gcn = self.ps.gcn(self.dims, self.dtype)
+        td = torch.float32 if self.dtype == "float32" else torch.float64
+        sizes = [w.size for w in model.weights]
+        self.n_params = int(sum(sizes))
+        self.wflat = torch.empty(self.n_params, dtype=td, device="cuda")
+        self.gflat = torch.zeros(self.n_params, dtype=td, device="cuda")
+        self.wviews, self.gviews = [], []
+        o = 0
+        for w in model.weights:
+            self.wviews.append(self.wflat[o:o + w.size].view(w.shape))
+            self.gviews.append(self.gflat[o:o + w.size].view(w.shape))
+            self.wviews[-1].copy_(torch.as_tensor(w, dtype=td))
+            o += w.size
+        self.wp = np.array([v.data_ptr() for v in self.wviews], dtype=np.uint64)
+        self.gp = np.array([v.data_ptr() for v in self.gviews], dtype=np.uint64)
+        if optimizer == "adam":
+            self.m = torch.zeros_like(self.wflat)
+            self.v = torch.zeros_like(self.wflat)
+            self.t = 0
+        self.epochs = epochs
+        self.ledger = torch.zeros((max(epochs, 1), self.k, self.L), dtype=torch.int64, device="cuda")
+        self.losses = torch.zeros((self.per_epoch, max(1, len(self.mine))), dtype=torch.float64,
+                                  device="cuda")
+        self.stream = D.current_stream()
+        self.dtc = DT[self.dtype]
+        self._workers = np.array(self.mine, dtype=np.int32)
+        self._states = np.zeros((max(1, len(self.mine)), 4), dtype=np.uint64)
+        self._boff = np.zeros(len(self.mine) + 1, dtype=np.int64)
+        self._bids = np.zeros(max(1, len(self.mine)) * max(1, batch_size), dtype=np.int64)
+        self._len = C.c_int64()
+
+    # -- one iteration (training.py:483-506) -------------------------------
+    def host_inputs(self, epoch, it):
+        """Batch ids and plan PCG64 states of this rank's workers (native host runtime)."""
+        o = 0
+        for i, w in enumerate(self.mine):
+            if self.sampler == "ladies":
+                tw = self.worker_train[w]
+                check(lib.skg_iteration_inputs(self.seed & 0xFFFFFFFFFFFFFFFF, epoch, it, w,
+                                               ptr(tw, C.c_int64), len(tw), self.batch_size,
+                                               ptr(self._bids[o:], C.c_int64), C.byref(self._len),
+                                               ptr(self._states[i], C.c_uint64)))
+                o += self._len.value
+                self._boff[i + 1] = o
+            else:
+                from .seeding import pcg64_state
+                self._states[i] = pcg64_state(self.seed, "plan", epoch, it, w)
+        return self._boff, self._bids, self._states
+
+    def sample(self):
+        n = len(self.mine)
+        if self.sampler == "ladies":
+            check(lib.skg_ladies_sample(self.ps.h, n, ptr(self._workers, C.c_int32),
+                                        ptr(self._boff, C.c_int64), ptr(self._bids, C.c_int64),
+                                        MODES[self.mode], float(self.cfg.skew_constant),
+                                        float(self.cfg.min_scale), ptr(self._states, C.c_uint64),
+                                        self.stream))
+        else:
+            check(lib.skg_saint_sample(self.ps.h, n, ptr(self._workers, C.c_int32), MODES[self.mode],
+                                       float(self.cfg.skew_constant), float(self.cfg.min_scale),
+                                       ptr(self._states, C.c_uint64), self.stream))
+
+    def compute(self, epoch, it):
+        check(lib.skg_zero(self.dtc, self.gflat.data_ptr(), self.n_params, self.stream))
+        for i in range(len(self.mine)):
+            check(lib.skg_gcn_step(self.gcn, i, ptr(self.wp, C.c_uint64), ptr(self.gp, C.c_uint64), 1,
+                                   self.losses[it % self.per_epoch, i].data_ptr(), self.stream))
+        if self.mine:
+            check(lib.skg_plans_ledger_add(self.ps.h, len(self.mine),
+                                           self.ledger[epoch % self.ledger.shape[0]].data_ptr(),
+                                           self.stream))
+
+    def reduce_and_step(self):
+        if self.world > 1:
+            self.dist.all_reduce(self.gflat)
+        contrib = float(len(self.active))
+        if self.optimizer == "sgd":
+            check(lib.skg_sgd_step(self.dtc, self.wflat.data_ptr(), self.gflat.data_ptr(),
+                                   self.n_params, float(self.lr), contrib, self.stream))
+        else:
+            self.t += 1
+            check(lib.skg_adam_step(self.dtc, self.wflat.data_ptr(), self.gflat.data_ptr(),
+                                    self.m.data_ptr(), self.v.data_ptr(), self.n_params,
+                                    float(self.lr), contrib, self.t, self.stream))
+
+    def iteration(self, epoch, it):
+        self.host_inputs(epoch, it)
+        self.sample()
+        self.compute(epoch, it)
+        self.reduce_and_step()
+
+    def check_errors(self):
+        for i in range(len(self.mine)):
+            _, info, rc = self.ps.stats(i)
+            check(rc)
+
+    def weights_to_model(self):
+        for w, v in zip(self.model.weights, self.wviews):
+            w[...] = v.double().cpu().numpy()
+
+    def close(self):
+        self.dg.release(self.ps)
+
+
+def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, cfg: SamplerConfig, *,
+                      epochs: int, batch_size: int, lr: float, mode: str, seed: int,
+                      sampler: str = "ladies", subgraph_size: int | None = None,
+                      optimizer: str = "sgd") -> tuple:
+    """Data-parallel training with per-iteration gradient averaging (training.py:430-518).
+
+    Single process: all workers run on this GPU.  Under torch.distributed (one process
+    per GPU) each rank runs a contiguous block of workers and gradients are summed with
+    an NCCL all-reduce; metrics and ledger are identical on every rank.
+    """
+    torch = _torch()
+    tr = Trainer(g, partition, model, cfg, batch_size=batch_size, lr=lr, mode=mode, seed=seed,
+                 sampler=sampler, subgraph_size=subgraph_size, optimizer=optimizer, epochs=epochs)
+    k, L = tr.k, tr.L
+    metrics = Metrics()
+    val_nodes = np.flatnonzero(g.val_mask) if g.val_mask is not None else np.empty(0, dtype=np.int64)
+    labels_t = torch.as_tensor(np.asarray(g.labels), device="cuda")
+    try:
+        for epoch in range(epochs):
+            for it in range(tr.per_epoch):
+                tr.iteration(epoch, it)
+            tr.check_errors()
+            losses = tr.losses.cpu().numpy()
+            ledger = tr.ledger[epoch]
+            loss_sum = np.zeros(k)
+            loss_cnt = np.zeros(k, dtype=np.int64)
+            for i, w in enumerate(tr.mine):  # python-float sums in iteration order
+                for it in range(tr.per_epoch):
+                    loss_sum[w] += losses[it, i]
+                    loss_cnt[w] += 1
+            if tr.world > 1:
+                ls = torch.as_tensor(loss_sum, device="cuda")
+                lc = torch.as_tensor(loss_cnt, device="cuda")
+                tr.dist.all_reduce(ls)
+                tr.dist.all_reduce(lc)
+                tr.dist.all_reduce(ledger)
+                loss_sum, loss_cnt = ls.cpu().numpy(), lc.cpu().numpy()
+            ledger_np = ledger.cpu().numpy()
+            logits = _predict_device(tr.dg, tr.wviews, tr.dims, tr.dtype)
+            preds = torch.argmax(logits, dim=1)
+            correct = (preds == labels_t).cpu().numpy()
+            val_acc = float(np.mean(correct[val_nodes])) if len(val_nodes) else 0.0
+            for w in range(k):
+                tw = tr.worker_train[w]
+                train_acc = float(np.mean(correct[tw])) if len(tw) else 0.0
+                mean_loss = float(loss_sum[w] / loss_cnt[w]) if loss_cnt[w] else 0.0
+                metrics.rows.append(MetricRow(epoch=epoch, worker=w, loss=mean_loss,
+                                              train_acc=train_acc, val_acc=val_acc,
+                                              comm_nodes_epoch=int(ledger_np[w].sum())))
+        tr.weights_to_model()
+        ledger_all = CommLedger(tr.ledger.cpu().numpy()[:epochs].copy())
+    finally:
+        tr.close()
+    return metrics, ledger_all

@@ -1,0 +1,106 @@
+"""Pin the CPU oracle against golden vectors produced by the unmodified reference."""
+
+import warnings
+
+import numpy as np
+import pytest
+
+import skewgcn_oracle as O
+from golden_util import (assert_plan_equal, cfg_for, golden, make_rng, oracle_graph_from_shaped,
+                         partition_for, plan_to_dict, shaped, shaped_batch, small_graph)
+
+G = golden("small")
+
+
+@pytest.mark.parametrize("case", G.cases("ladies"))
+def test_ladies_small(case):
+    m = G.meta[case]
+    g = small_graph(m["graph"])
+    part = partition_for(m, g.n_nodes)
+    plan = O.ladies_plan(g, part, m["worker"], np.array(m["batch"], dtype=np.int64), cfg_for(m),
+                         m["n_layers"], make_rng(m["rng"]))
+    assert_plan_equal(plan_to_dict(plan), G.expected_plan(case))
+
+
+@pytest.mark.parametrize("case", G.cases("saint"))
+def test_saint_small(case):
+    m = G.meta[case]
+    g = small_graph(m["graph"])
+    part = partition_for(m, g.n_nodes)
+    train = np.array(m["train"], dtype=np.int64)
+    norms = O.column_norms(g, train, train) if m["precomputed"] else None
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        plan = O.saint_plan(g, part, m["worker"], train, m["size"], cfg_for(m), m["n_layers"],
+                            make_rng(m["rng"]), norms=norms)
+    assert_plan_equal(plan_to_dict(plan), G.expected_plan(case))
+
+
+@pytest.mark.parametrize("case", G.cases("fb"))
+def test_forward_backward_small(case):
+    m = G.meta[case]
+    g = small_graph(m["graph"])
+    part = partition_for(m, g.n_nodes)
+    plan = O.ladies_plan(g, part, m["worker"], np.array(m["batch"], dtype=np.int64), cfg_for(m),
+                         m["n_layers"], make_rng(m["rng"]))
+    assert_plan_equal(plan_to_dict(plan), G.expected_plan(case))
+    x = G.get(case, "features")
+    y = G.get(case, "labels")
+    ws = O.init_model(m["dims"], m["model_seed"])
+    loss, grads = O.loss_and_backward(ws, plan, x, y)
+    np.testing.assert_allclose(O.forward(ws, plan, x), G.get(case, "logits"), rtol=1e-12,
+                               atol=1e-14)
+    assert loss == pytest.approx(float(G.get(case, "loss")), rel=1e-12)
+    for l, gr in enumerate(grads):
+        np.testing.assert_allclose(gr, G.get(case, f"grad{l}"), rtol=1e-10, atol=1e-14)
+
+
+@pytest.mark.parametrize("case", G.cases("train"))
+def test_train_distributed_small(case):
+    m = G.meta[case]
+    g = O.Graph(n_nodes=m["n"], offsets=G.get(case, "offsets"), neighbors=G.get(case, "neighbors"),
+                weights=G.get(case, "weights"), normalized=True, features=G.get(case, "features"),
+                labels=G.get(case, "labels"), train_mask=G.get(case, "train_mask"),
+                val_mask=G.get(case, "val_mask"))
+    part = O.partition_nodes(m["n"], m["k"], "random", seed=m["pseed"])
+    ws = O.init_model(m["dims"], m["model_seed"])
+    cfg = O.SamplerConfig(budget=m["budget"], skew_constant=m["D"], mode=m["mode"])
+    rows, ledger = O.train_distributed(g, part, ws, cfg, epochs=m["epochs"],
+                                       batch_size=m["batch_size"], lr=m["lr"], mode=m["mode"],
+                                       seed=m["seed"], sampler=m["sampler"],
+                                       subgraph_size=m["subgraph_size"], optimizer=m["optimizer"])
+    np.testing.assert_array_equal(ledger, G.get(case, "ledger"))
+    got = np.array([[r.epoch, r.worker, r.loss, r.train_acc, r.val_acc, r.comm_nodes_epoch]
+                    for r in rows])
+    np.testing.assert_allclose(got, G.get(case, "metrics"), rtol=1e-9, atol=1e-12)
+    for l, w in enumerate(ws):
+        np.testing.assert_allclose(w, G.get(case, f"w{l}"), rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("shape", ["cora", "reddit_s", "amazon_s"])
+def test_shaped_plans(shape):
+    G2 = golden(shape)
+    gm = G2.meta[f"shape_{shape}"]
+    sgph = shaped(shape)
+    assert sgph.structure_hash() == gm["structure_sha"], "generator drifted from the golden graph"
+    g = oracle_graph_from_shaped(sgph)
+    cases = G2.cases("shaped_ladies") + G2.cases("shaped_saint")
+    assert cases
+    part = None
+    saint_norms = None
+    for case in cases:
+        m = G2.meta[case]
+        if part is None:
+            part = O.partition_nodes(g.n_nodes, m["k"], "random", seed=m["pseed"])
+        cfg = O.SamplerConfig(budget=m["budget"], skew_constant=m["D"], mode=m["mode"])
+        rng = O.spawn_rng(m["seed"], "plan", m["epoch"], m["it"], m["worker"])
+        if m["kind"] == "shaped_ladies":
+            batch = shaped_batch(g, part, m)
+            plan = O.ladies_plan(g, part, m["worker"], batch, cfg, m["n_layers"], rng)
+        else:
+            train = np.flatnonzero(g.train_mask)
+            if saint_norms is None and m["mode"] != "local":
+                saint_norms = O.column_norms(g, train, train)
+            plan = O.saint_plan(g, part, m["worker"], train, m["budget"], cfg, m["n_layers"], rng,
+                                norms=None if m["mode"] == "local" else saint_norms)
+        assert_plan_equal(plan_to_dict(plan), G2.expected_plan(case))
