@@ -135,6 +135,10 @@ int skg_gcn_destroy(skg_gcn* g);
 /* forward + loss + backward; grads (device) += or = dW_l; loss_dev: one double. */
 int skg_gcn_step(skg_gcn* g, int slot, const uint64_t* weight_ptrs, const uint64_t* grad_ptrs,
                  int accumulate, uint64_t loss_dev, void* stream);
+/* All slots [slot0, slot0+n) in one batched launch per stage; grads (+)= sum over the
+ * slots in slot order; loss_dev receives n doubles. */
+int skg_gcn_step_batch(skg_gcn* g, int slot0, int n, const uint64_t* weight_ptrs,
+                       const uint64_t* grad_ptrs, int accumulate, uint64_t loss_dev, void* stream);
 int skg_gcn_forward(skg_gcn* g, int slot, const uint64_t* weight_ptrs, void* stream);
 /* Synchronous: copies logits of the last forward (rows x dims[L], unpadded, in the gcn
  * dtype) to host; rows_out receives the batch size. */

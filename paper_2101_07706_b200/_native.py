@@ -71,6 +71,7 @@ _sig("skg_plan_layer", C.c_int, vp, C.c_int, C.c_int, P(i32), P(i32), P(i32), P(
 _sig("skg_gcn_create", C.c_int, vp, C.c_int, P(i64), C.c_int, P(vp))
 _sig("skg_gcn_destroy", C.c_int, vp)
 _sig("skg_gcn_step", C.c_int, vp, C.c_int, P(u64), P(u64), C.c_int, u64, vp)
+_sig("skg_gcn_step_batch", C.c_int, vp, C.c_int, C.c_int, P(u64), P(u64), C.c_int, u64, vp)
 _sig("skg_gcn_forward", C.c_int, vp, C.c_int, P(u64), vp)
 _sig("skg_gcn_read_logits", C.c_int, vp, C.c_int, vp, P(i64))
 _sig("skg_predict_logits", C.c_int, vp, C.c_int, P(i64), P(u64), C.c_int, u64, vp)
@@ -87,7 +88,7 @@ EXPORTED = [
     "skg_ctx_set_labels", "skg_ctx_set_owner", "skg_ctx_info", "skg_plans_ledger_add", "skg_ipc_handle", "skg_ipc_open", "skg_ipc_close",
     "skg_plans_create", "skg_plans_destroy", "skg_ladies_sample", "skg_ladies_sample_device", "skg_saint_set_candidates",
     "skg_saint_sample", "skg_plan_stats", "skg_plan_layer", "skg_gcn_create", "skg_gcn_destroy",
-    "skg_gcn_step", "skg_gcn_forward", "skg_gcn_read_logits", "skg_predict_logits",
+    "skg_gcn_step", "skg_gcn_step_batch", "skg_gcn_forward", "skg_gcn_read_logits", "skg_predict_logits",
     "skg_sgd_step", "skg_adam_step", "skg_zero", "skg_debug_reduce",
 ]
 

@@ -1,5 +1,6 @@
 // extern "C" boundary (include/skewgcn_b200.h): graph store, plan arenas, orchestration.
 #include <algorithm>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -114,19 +115,24 @@ struct skg_plans {
   std::vector<bool> local_norm_ready;
 };
 
-struct GcnSlot {
-  char* X0 = nullptr;
-  std::vector<char*> U, H;
-  char* G0 = nullptr;
-  char* G1 = nullptr;
-};
 struct skg_gcn {
   skg_plans* ps = nullptr;
   int L = 0, dtype = DT_F32;
   std::vector<int64_t> dims, ld;
-  std::vector<GcnSlot> slots;
+  int64_t ld_max = 0, R = 0;
+  int n_slots = 0;
   char* arena = nullptr;
-  int64_t ld_max = 0;
+  // layer-major activations: slot z of buffer X at X + z * R * ld(X) elements
+  char* X0 = nullptr;
+  std::vector<char*> U, H;
+  char* G0 = nullptr;
+  char* G1 = nullptr;
+  char* parts = nullptr;  // split-K partials of dW, one d_l x d_{l+1} block per slot
+  int64_t part_elems = 0;
+  double* row_loss = nullptr;
+  LayerDesc* d_layers = nullptr;      // [L][n_slots]
+  SlotDesc* d_slots = nullptr;        // [n_slots]
+  const int32_t** d_rows = nullptr;   // [L][n_slots] -> |S_{l+1}| scalars
 };
 
 // ------------------------------------------------------------------ small kernels
@@ -500,6 +506,7 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     cv.add(P.word_prefix, n_words);
     cv.add(P.tile_a, cap_tiles);
     cv.add(P.tile_b, cap_tiles);
+    cv.add(P.tile_c, cap_tiles);
     cv.add(P.bucket_off, kind == KIND_LADIES ? cap_cand + 1 : 1);
     cv.add(P.bucket_r, kind == KIND_LADIES ? cap_pairs : 1);
     cv.add(P.bucket_w, kind == KIND_LADIES ? cap_pairs : 1);
@@ -898,28 +905,67 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   g->ps = ps;
   g->L = L;
   g->dtype = dtype;
+  g->n_slots = ps->n_slots;
   g->dims.assign(dims, dims + L + 1);
   g->ld.resize(L + 1);
+  int64_t wmax = 0;
   for (int l = 0; l <= L; ++l) {
     g->ld[l] = round4(dims[l]);
     g->ld_max = std::max(g->ld_max, g->ld[l]);
+    if (l < L) wmax = std::max(wmax, dims[l] * dims[l + 1]);
   }
   const size_t es = dtype == DT_F32 ? 4 : 8;
-  const size_t R = ps->cap_rows;
+  const int64_t R = ps->cap_rows, S = ps->n_slots;
+  g->R = R;
+  g->part_elems = wmax;
+  g->U.resize(L);
+  g->H.resize(L + 1);
   Carver cv;
-  g->slots.resize(ps->n_slots);
-  for (auto& s : g->slots) {
-    s.U.resize(L);
-    s.H.resize(L + 1);
-    cv.add(s.X0, R * g->ld[0] * es);
-    for (int l = 0; l < L; ++l) cv.add(s.U[l], R * g->ld[l] * es);
-    for (int l = 1; l <= L; ++l) cv.add(s.H[l], R * g->ld[l] * es);
-    cv.add(s.G0, R * g->ld_max * es);
-    cv.add(s.G1, R * g->ld_max * es);
-  }
+  cv.add(g->X0, (size_t)S * R * g->ld[0] * es);
+  for (int l = 0; l < L; ++l) cv.add(g->U[l], (size_t)S * R * g->ld[l] * es);
+  for (int l = 1; l <= L; ++l) cv.add(g->H[l], (size_t)S * R * g->ld[l] * es);
+  cv.add(g->G0, (size_t)S * R * g->ld_max * es);
+  cv.add(g->G1, (size_t)S * R * g->ld_max * es);
+  cv.add(g->parts, (size_t)S * wmax * es);
+  cv.add(g->row_loss, (size_t)S * R);
+  cv.add(g->d_layers, (size_t)L * S);
+  cv.add(g->d_slots, (size_t)S);
+  cv.add(g->d_rows, (size_t)L * S);
   CK(cudaMalloc(&g->arena, cv.off));
   CK(cudaMemset(g->arena, 0, cv.off));
   cv.bind(g->arena);
+  // descriptors: pointers into the plan arena are fixed for the plan set's lifetime
+  std::vector<LayerDesc> hl((size_t)L * S);
+  std::vector<const int32_t*> hr((size_t)L * S);
+  std::vector<SlotDesc> hs(S);
+  for (int z = 0; z < S; ++z) {
+    const PlanDev& P = ps->h[z];
+    for (int l = 0; l < L; ++l) {
+      const int t = ps->kind == KIND_LADIES ? L - 1 - l : 0;
+      LayerDesc d;
+      d.rows = &P.stat[t].n_upper;
+      d.cols = &P.stat[t].n_nodes;
+      d.indptr = P.indptr + (size_t)t * (P.cap_rows + 1);
+      d.indices = P.indices + (size_t)t * P.cap_pairs;
+      d.val = P.val + (size_t)t * P.cap_pairs;
+      d.tindptr = P.tindptr + (size_t)t * (P.cap_rows + 1);
+      d.tindices = P.tindices + (size_t)t * P.cap_pairs;
+      d.tval = P.tval + (size_t)t * P.cap_pairs;
+      hl[(size_t)l * S + z] = d;
+      hr[(size_t)l * S + z] = d.rows;
+    }
+    const int t0 = ps->kind == KIND_LADIES ? L - 1 : 0;
+    SlotDesc sd;
+    sd.in_nodes = P.nodes + (size_t)t0 * P.cap_rows;
+    sd.n_in = &P.stat[t0].n_nodes;
+    sd.batch = ps->kind == KIND_LADIES ? nullptr : P.nodes;  // LADIES: set per sampling call
+    sd.n_batch = ps->kind == KIND_LADIES ? &P.stat[0].n_upper : &P.stat[0].n_nodes;
+    sd.err = P.err;
+    hs[z] = sd;
+  }
+  CK(cudaMemcpy(g->d_layers, hl.data(), sizeof(LayerDesc) * hl.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(g->d_rows, hr.data(), sizeof(void*) * hr.size(), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(g->d_slots, hs.data(), sizeof(SlotDesc) * hs.size(), cudaMemcpyHostToDevice));
   *out = g;
   return SKG_OK;
 }
@@ -932,74 +978,95 @@ extern "C" int skg_gcn_destroy(skg_gcn* g) {
 }
 
 namespace {
-struct LayerView {
-  const int32_t* d_rows;  // |S_{l+1}|
-  const int32_t* d_cols;  // |S_l|
-  const int32_t *indptr, *indices, *tindptr, *tindices;
-  const double *val, *tval;
-};
-LayerView layer_view(const skg_plans* ps, int slot, int l) {
-  const PlanDev& P = ps->h[slot];
-  const int t = ps->kind == KIND_LADIES ? ps->L - 1 - l : 0;
-  LayerView v;
-  v.d_rows = &P.stat[t].n_upper;
-  v.d_cols = &P.stat[t].n_nodes;
-  v.indptr = P.indptr + (size_t)t * (P.cap_rows + 1);
-  v.indices = P.indices + (size_t)t * P.cap_pairs;
-  v.val = P.val + (size_t)t * P.cap_pairs;
-  v.tindptr = P.tindptr + (size_t)t * (P.cap_rows + 1);
-  v.tindices = P.tindices + (size_t)t * P.cap_pairs;
-  v.tval = P.tval + (size_t)t * P.cap_pairs;
-  return v;
+// LADIES batch pointers change with every sampling call (they point at the caller's
+// batch buffer); refresh them in the slot descriptors before running.
+int refresh_batches(skg_gcn* g, int z0, int n, cudaStream_t st) {
+  skg_plans* ps = g->ps;
+  if (ps->kind != KIND_LADIES) return SKG_OK;
+  for (int z = z0; z < z0 + n; ++z) {
+    const int32_t* b = ps->h[z].batch;
+    CK(cudaMemcpyAsync(reinterpret_cast<char*>(g->d_slots + z) + offsetof(SlotDesc, batch), &b,
+                       sizeof(b), cudaMemcpyHostToDevice, st));
+  }
+  return SKG_OK;
 }
 
 template <typename T>
-int gcn_run(skg_gcn* g, int slot, const uint64_t* wp, const uint64_t* gp, bool acc, double* loss,
-            bool backward, cudaStream_t st) {
+Act<T> act(char* base, int64_t R, int64_t ld_alloc, int64_t ld, int z0, size_t es = sizeof(T)) {
+  Act<T> a;
+  a.base = reinterpret_cast<T*>(base) + (int64_t)z0 * R * ld_alloc;
+  a.stride = R * ld_alloc;
+  a.ld = ld;
+  return a;
+}
+
+template <typename T>
+int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, bool accum,
+            double* loss, bool backward, cudaStream_t st) {
   skg_plans* ps = g->ps;
   skg_ctx* c = ps->ctx;
-  const PlanDev& P = ps->h[slot];
-  GcnSlot& S = g->slots[slot];
-  const int L = g->L;
-  const int R = ps->cap_rows;
-  auto W = [&](int l) { return reinterpret_cast<const T*>(wp[l]); };
-  // layer-0 input rows X[S_0] (local shard or NVLink peer shards)
-  LayerView v0 = layer_view(ps, slot, 0);
-  const int t0 = ps->kind == KIND_LADIES ? L - 1 : 0;
-  const int32_t* in_nodes = P.nodes + (size_t)t0 * P.cap_rows;
-  T* X0 = reinterpret_cast<T*>(S.X0);
-  gather_rows<T>(c->fstore(), in_nodes, v0.d_cols, R, X0, g->ld[0], st);
+  const int L = g->L, S = g->n_slots;
+  const int64_t R = g->R;
+  const int Ri = (int)R;
+  int rc = refresh_batches(g, z0, n, st);
+  if (rc) return rc;
+  auto W = [&](int l) {
+    Act<T> a;
+    a.base = reinterpret_cast<T*>(wp[l]);
+    a.stride = 0;
+    a.ld = g->dims[l + 1];
+    return a;
+  };
+  Act<T> X0 = act<T>(g->X0, R, g->ld[0], g->ld[0], z0);
+  gather_rows_b<T>(c->fstore(), g->d_slots + z0, n, Ri, X0, st);
   for (int l = 0; l < L; ++l) {
-    LayerView v = layer_view(ps, slot, l);
-    const T* A = l == 0 ? X0 : reinterpret_cast<const T*>(S.H[l]);
-    T* U = reinterpret_cast<T*>(S.U[l]);
-    spmm<T>(v.d_rows, R, v.indptr, v.indices, v.val, A, g->ld[l], l > 0, U, g->ld[l], g->ld[l], st);
-    gemm<T>(false, false, R, (int)g->dims[l + 1], (int)g->dims[l], v.d_rows, nullptr, U, g->ld[l],
-            W(l), g->dims[l + 1], reinterpret_cast<T*>(S.H[l + 1]), g->ld[l + 1], false, st);
+    const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
+    Act<T> A = l == 0 ? X0 : act<T>(g->H[l], R, g->ld[l], g->ld[l], z0);
+    Act<T> U = act<T>(g->U[l], R, g->ld[l], g->ld[l], z0);
+    spmm_b<T>(lds, n, Ri, false, l > 0, A, A, U, g->ld[l], st);
+    Act<T> Hn = act<T>(g->H[l + 1], R, g->ld[l + 1], g->ld[l + 1], z0);
+    gemm_b<T>(false, false, n, Ri, (int)g->dims[l + 1], (int)g->dims[l],
+              g->d_rows + (size_t)l * S + z0, nullptr, U, W(l), Hn, false, st);
   }
   if (!backward) return SKG_OK;
-  // loss over the batch rows (training.py:293-308)
-  LayerView vt = layer_view(ps, slot, L - 1);
-  const int32_t* batch = ps->kind == KIND_LADIES ? P.batch : P.nodes;
-  T* G = reinterpret_cast<T*>(S.G0);
-  T* Gu = reinterpret_cast<T*>(S.G1);
-  softmax_ce<T>(vt.d_rows, R, batch, c->d_labels, reinterpret_cast<const T*>(S.H[L]), g->ld[L],
-                (int)g->dims[L], G, g->ld[L], loss, P.err, st);
-  int64_t ldG = g->ld[L];
+  Act<T> G = act<T>(g->G0, R, g->ld_max, g->ld[L], z0);
+  Act<T> Gu = act<T>(g->G1, R, g->ld_max, g->ld[L], z0);
+  softmax_ce_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
+                  (int)g->dims[L], G, g->row_loss + (size_t)z0 * R, loss, st);
   for (int l = L - 1; l >= 0; --l) {
-    LayerView v = layer_view(ps, slot, l);
-    // dW_l = U_l^T G  (K = |S_{l+1}| read on device)
-    gemm<T>(true, false, (int)g->dims[l], (int)g->dims[l + 1], R, nullptr, v.d_rows,
-            reinterpret_cast<const T*>(S.U[l]), g->ld[l], G, ldG, reinterpret_cast<T*>(gp[l]),
-            g->dims[l + 1], acc, st);
+    const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
+    const int32_t* const* rows = g->d_rows + (size_t)l * S + z0;
+    const int dl = (int)g->dims[l], dn = (int)g->dims[l + 1];
+    // dW_l = sum_slots U_l^T G (split-K over slots, reduced in slot order)
+    Act<T> P;
+    P.base = reinterpret_cast<T*>(g->parts);
+    P.stride = g->part_elems;
+    P.ld = dn;
+    gemm_b<T>(true, false, n, dl, dn, Ri, nullptr, rows, act<T>(g->U[l], R, g->ld[l], g->ld[l], z0), G,
+              P, false, st);
+    reduce_slots<T>(P.base, P.stride, n, dl, dn, dn, reinterpret_cast<T*>(gp[l]), dn, accum, st);
     if (l == 0) break;
-    // G_u = G W_l^T
-    gemm<T>(false, true, R, (int)g->dims[l], (int)g->dims[l + 1], v.d_rows, nullptr, G, ldG, W(l),
-            g->dims[l + 1], Gu, g->ld[l], false, st);
-    // G_prev = (Block_l^T G_u) * [H_l > 0]
-    spmm_t_mask<T>(v.d_cols, R, v.tindptr, v.tindices, v.tval, Gu, g->ld[l],
-                   reinterpret_cast<const T*>(S.H[l]), g->ld[l], G, g->ld[l], g->ld[l], st);
-    ldG = g->ld[l];
+    // G_u = G W_l^T ; G <- (Block_l^T G_u) * [H_l > 0]
+    Gu.ld = g->ld[l];
+    gemm_b<T>(false, true, n, Ri, dl, dn, rows, nullptr, G, W(l), Gu, false, st);
+    Act<T> Gn = G;
+    Gn.ld = g->ld[l];
+    spmm_b<T>(lds, n, Ri, true, false, Gu, act<T>(g->H[l], R, g->ld[l], g->ld[l], z0), Gn,
+              g->ld[l], st);
+    G = Gn;
+  }
+  return SKG_OK;
+}
+
+int gcn_dispatch(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, bool acc,
+                 double* loss, bool backward, cudaStream_t st) {
+  int rc = g->dtype == DT_F32 ? gcn_run<float>(g, z0, n, wp, gp, acc, loss, backward, st)
+                              : gcn_run<double>(g, z0, n, wp, gp, acc, loss, backward, st);
+  if (rc) return rc;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("gcn: ") + cudaGetErrorString(e));
+    return SKG_ERR_CUDA;
   }
   return SKG_OK;
 }
@@ -1007,39 +1074,32 @@ int gcn_run(skg_gcn* g, int slot, const uint64_t* wp, const uint64_t* gp, bool a
 
 extern "C" int skg_gcn_step(skg_gcn* g, int slot, const uint64_t* wp, const uint64_t* gp,
                             int accumulate, uint64_t loss_dev, void* stream) {
-  ARG(g && slot >= 0 && slot < g->ps->n_slots && wp && gp && loss_dev, "bad gcn_step arguments");
+  ARG(g && slot >= 0 && slot < g->n_slots && wp && gp && loss_dev, "bad gcn_step arguments");
   ARG(g->ps->ctx->d_labels, "labels not set");
   CK(cudaSetDevice(g->ps->ctx->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  int rc = g->dtype == DT_F32
-               ? gcn_run<float>(g, slot, wp, gp, accumulate != 0, (double*)loss_dev, true, st)
-               : gcn_run<double>(g, slot, wp, gp, accumulate != 0, (double*)loss_dev, true, st);
-  if (rc) return rc;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_error(std::string("gcn_step: ") + cudaGetErrorString(e));
-    return SKG_ERR_CUDA;
-  }
-  return SKG_OK;
+  return gcn_dispatch(g, slot, 1, wp, gp, accumulate != 0, (double*)loss_dev, true,
+                      (cudaStream_t)stream);
+}
+
+extern "C" int skg_gcn_step_batch(skg_gcn* g, int slot0, int n, const uint64_t* wp,
+                                  const uint64_t* gp, int accumulate, uint64_t loss_dev,
+                                  void* stream) {
+  ARG(g && slot0 >= 0 && n >= 1 && slot0 + n <= g->n_slots && wp && gp && loss_dev,
+      "bad gcn_step_batch arguments");
+  ARG(g->ps->ctx->d_labels, "labels not set");
+  CK(cudaSetDevice(g->ps->ctx->device));
+  return gcn_dispatch(g, slot0, n, wp, gp, accumulate != 0, (double*)loss_dev, true,
+                      (cudaStream_t)stream);
 }
 
 extern "C" int skg_gcn_forward(skg_gcn* g, int slot, const uint64_t* wp, void* stream) {
-  ARG(g && slot >= 0 && slot < g->ps->n_slots && wp, "bad gcn_forward arguments");
+  ARG(g && slot >= 0 && slot < g->n_slots && wp, "bad gcn_forward arguments");
   CK(cudaSetDevice(g->ps->ctx->device));
-  cudaStream_t st = (cudaStream_t)stream;
-  int rc = g->dtype == DT_F32 ? gcn_run<float>(g, slot, wp, nullptr, false, nullptr, false, st)
-                              : gcn_run<double>(g, slot, wp, nullptr, false, nullptr, false, st);
-  if (rc) return rc;
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    set_error(std::string("gcn_forward: ") + cudaGetErrorString(e));
-    return SKG_ERR_CUDA;
-  }
-  return SKG_OK;
+  return gcn_dispatch(g, slot, 1, wp, nullptr, false, nullptr, false, (cudaStream_t)stream);
 }
 
 extern "C" int skg_gcn_read_logits(skg_gcn* g, int slot, void* host_out, int64_t* rows_out) {
-  ARG(g && slot >= 0 && slot < g->ps->n_slots, "bad slot");
+  ARG(g && slot >= 0 && slot < g->n_slots, "bad slot");
   CK(cudaSetDevice(g->ps->ctx->device));
   CK(cudaDeviceSynchronize());
   skg_plans* ps = g->ps;
@@ -1050,9 +1110,9 @@ extern "C" int skg_gcn_read_logits(skg_gcn* g, int slot, void* host_out, int64_t
   *rows_out = rows;
   const size_t es = g->dtype == DT_F32 ? 4 : 8;
   const int64_t C = g->dims[g->L];
+  const char* src = g->H[g->L] + (size_t)slot * g->R * g->ld[g->L] * es;
   if (host_out && rows)
-    CK(cudaMemcpy2D(host_out, es * C, g->slots[slot].H[g->L], es * g->ld[g->L], es * C, rows,
-                    cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy2D(host_out, es * C, src, es * g->ld[g->L], es * C, rows, cudaMemcpyDeviceToHost));
   return SKG_OK;
 }
 
@@ -1078,15 +1138,14 @@ extern "C" int skg_predict_logits(skg_ctx* c, int L, const int64_t* dims, const 
     if (dtype == DT_F32) {
       const float* A = l == 0 ? (const float*)c->d_x : (const float*)H;
       spmm_full<float>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (float*)U, ldl, ldl, st);
-      gemm<float>(false, false, (int)c->n, (int)dims[l + 1], (int)dims[l], nullptr, nullptr,
-                  (const float*)U, ldl, (const float*)wp[l], dims[l + 1],
-                  last ? (float*)out_dev : (float*)H, ldo, false, st);
+      gemm_plain<float>((int)c->n, (int)dims[l + 1], (int)dims[l], (const float*)U, ldl,
+                        (const float*)wp[l], dims[l + 1], last ? (float*)out_dev : (float*)H, ldo, st);
     } else {
       const double* A = l == 0 ? (const double*)c->d_x : (const double*)H;
       spmm_full<double>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (double*)U, ldl, ldl, st);
-      gemm<double>(false, false, (int)c->n, (int)dims[l + 1], (int)dims[l], nullptr, nullptr,
-                   (const double*)U, ldl, (const double*)wp[l], dims[l + 1],
-                   last ? (double*)out_dev : (double*)H, ldo, false, st);
+      gemm_plain<double>((int)c->n, (int)dims[l + 1], (int)dims[l], (const double*)U, ldl,
+                         (const double*)wp[l], dims[l + 1], last ? (double*)out_dev : (double*)H, ldo,
+                         st);
     }
   }
   CK(cudaStreamSynchronize(st));

@@ -1,11 +1,13 @@
-// GCN compute over a sampled plan: fused feature gather (local shard or NVLink peer),
-// CSR SpMM (ReLU fused on the input), transposed SpMM fused with the ReLU mask, a tiled
-// GEMM for H·W, softmax cross-entropy forward+backward and the optimizer steps.
+// GCN compute over sampled plans: fused feature gather (local shard or NVLink peer),
+// CSR SpMM (ReLU fused on the input), transposed SpMM fused with the ReLU mask, tiled
+// GEMMs for H·W, softmax cross-entropy forward+backward and the optimizer steps.
+// Every stage handles all plans (slots) of an iteration in one launch.
 //
 // Reference: training.py:261-318 (forward / loss_and_backward), 398-427 (SGD / Adam),
 // 325-334 (predict_logits).  Activation rows are padded to a multiple of 4 elements so
 // every row access is a 16-byte vector; padding columns stay zero.
 #include <cub/block/block_reduce.cuh>
+#include <algorithm>
 #include <cstdio>
 
 #include "gcn.cuh"
@@ -69,72 +71,72 @@ static int sms() {
   return n;
 }
 
+static int row_blocks(int max_rows, int n) {
+  // warp per row, 8 warps per CTA; cover all rows but keep >= ~2 waves overall
+  int b = (max_rows + 7) / 8;
+  int cap = std::max(1, (4 * sms() + n - 1) / n);
+  return std::max(1, std::min(b, std::max(cap, 1)));
+}
+
 // ------------------------------------------------------------------ gather (K7)
+// X0[slot][c] = X[S_0[c]] from the owner's shard (local or NVLink peer pointer).
 template <typename T>
-__global__ void k_gather(FeatStore fs, const int32_t* ids, const int32_t* d_n, T* out, int64_t ldo) {
-  const int n = *d_n;
+__global__ void k_gather_b(FeatStore fs, const SlotDesc* sd, Act<T> out) {
+  const SlotDesc d = sd[blockIdx.y];
+  const int n = *d.n_in;
+  T* o = out.at(blockIdx.y);
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
-    const int node = ids[r];
+    const int node = d.in_nodes[r];
     const int rank = fs.node_rank ? fs.node_rank[node] : 0;
     const int64_t row = fs.node_row ? fs.node_row[node] : node;
     const T* src = reinterpret_cast<const T*>(fs.shards[rank]) + row * fs.ld;
-    for (int64_t c = lane * 4; c < fs.ld; c += 128) Vec4<T>::load(src + c).store(out + r * ldo + c);
+    for (int64_t c = lane * 4; c < fs.ld; c += 128) Vec4<T>::load(src + c).store(o + r * out.ld + c);
   }
 }
 
 template <typename T>
-void gather_rows(const FeatStore& fs, const int32_t* ids, const int32_t* d_n, int max_n, T* out,
-                 int64_t ldo, cudaStream_t st) {
-  int blocks = std::max(1, std::min((max_n + 7) / 8, 4 * sms()));
-  GLAUNCH(k_gather<T><<<blocks, 256, 0, st>>>(fs, ids, d_n, out, ldo));
+void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows, Act<T> out,
+                   cudaStream_t st) {
+  GLAUNCH(k_gather_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(fs, sd, out));
 }
 
 // ------------------------------------------------------------------ SpMM (K8 / K10)
-template <typename T, bool RELU, bool MASK>
-__global__ void k_spmm(const int32_t* d_rows, const int32_t* __restrict__ indptr,
-                       const int32_t* __restrict__ indices, const double* __restrict__ val,
-                       const T* __restrict__ A, int64_t lda, const T* __restrict__ H, int64_t ldh,
-                       T* __restrict__ out, int64_t ldo, int64_t width) {
-  const int rows = *d_rows;
+template <typename T, bool TRANS, bool RELU>
+__global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, int64_t width) {
+  const LayerDesc d = lds[blockIdx.y];
+  const int rows = TRANS ? *d.cols : *d.rows;
+  const int32_t* __restrict__ ip = TRANS ? d.tindptr : d.indptr;
+  const int32_t* __restrict__ ix = TRANS ? d.tindices : d.indices;
+  const double* __restrict__ vv = TRANS ? d.tval : d.val;
+  const T* a = A.at(blockIdx.y);
+  const T* h = TRANS ? H.at(blockIdx.y) : nullptr;
+  T* o = out.at(blockIdx.y);
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
   for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
-    const int b = indptr[r], e = indptr[r + 1];
+    const int b = ip[r], e = ip[r + 1];
     for (int64_t c = lane * 4; c < width; c += 128) {
       Vec4<T> acc = Vec4<T>::zero();
       for (int p = b; p < e; ++p) {
-        Vec4<T> x = Vec4<T>::load(A + (int64_t)indices[p] * lda + c);
+        Vec4<T> x = Vec4<T>::load(a + (int64_t)ix[p] * A.ld + c);
         if (RELU) x.relu();
-        acc.fma((T)val[p], x);
+        acc.fma((T)vv[p], x);
       }
-      if (MASK) acc.mask(Vec4<T>::load(H + (int64_t)r * ldh + c));
-      acc.store(out + (int64_t)r * ldo + c);
+      if (TRANS) acc.mask(Vec4<T>::load(h + (int64_t)r * H.ld + c));
+      acc.store(o + (int64_t)r * out.ld + c);
     }
   }
 }
 
 template <typename T>
-void spmm(const int32_t* d_rows, int max_rows, const int32_t* indptr, const int32_t* indices,
-          const double* val, const T* A, int64_t lda, bool relu_in, T* out, int64_t ldo,
-          int64_t width, cudaStream_t st) {
-  int blocks = std::max(1, std::min((max_rows + 7) / 8, 4 * sms()));
-  if (relu_in)
-    GLAUNCH((k_spmm<T, true, false><<<blocks, 256, 0, st>>>(d_rows, indptr, indices, val, A, lda,
-                                                            nullptr, 0, out, ldo, width)));
-  else
-    GLAUNCH((k_spmm<T, false, false><<<blocks, 256, 0, st>>>(d_rows, indptr, indices, val, A, lda,
-                                                             nullptr, 0, out, ldo, width)));
-}
-
-template <typename T>
-void spmm_t_mask(const int32_t* d_rows, int max_rows, const int32_t* indptr,
-                 const int32_t* indices, const double* val, const T* G, int64_t ldg,
-                 const T* H, int64_t ldh, T* out, int64_t ldo, int64_t width, cudaStream_t st) {
-  int blocks = std::max(1, std::min((max_rows + 7) / 8, 4 * sms()));
-  GLAUNCH((k_spmm<T, false, true><<<blocks, 256, 0, st>>>(d_rows, indptr, indices, val, G, ldg, H,
-                                                          ldh, out, ldo, width)));
+void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
+            Act<T> H, Act<T> out, int64_t width, cudaStream_t st) {
+  dim3 grid(row_blocks(max_rows, n), n);
+  if (transposed) GLAUNCH((k_spmm_b<T, true, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
+  else if (relu_in) GLAUNCH((k_spmm_b<T, false, true><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
+  else GLAUNCH((k_spmm_b<T, false, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
 }
 
 // full-graph SpMM for predict_logits (int64 offsets)
@@ -169,142 +171,212 @@ void spmm_full(int64_t n, const int64_t* off, const int32_t* col, const double* 
 }
 
 // ------------------------------------------------------------------ GEMM (K9)
-// 64x64x16 tiles, 256 threads, 4x4 outputs per thread; op(A) is M x K, op(B) is K x N.
-constexpr int GBM = 64, GBN = 64, GBK = 16;
-
-template <typename T, bool TA, bool TB>
-__global__ void __launch_bounds__(256) k_gemm(int M, int N, int K, const int32_t* dM, const int32_t* dK,
-                                              const T* __restrict__ A, int64_t lda,
-                                              const T* __restrict__ B, int64_t ldb,
-                                              T* __restrict__ C, int64_t ldc, bool accumulate) {
-  if (dM) M = *dM;
-  if (dK) K = *dK;
-  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+// Register-tiled SIMT GEMM, BMxBN tile per CTA, TMxTN outputs per thread, slot on
+// blockIdx.z.  op(A) is M x K, op(B) is K x N (TA/TB select transposed storage).
+template <typename T, bool TA, bool TB, int BM, int BN, int BK, int TM, int TN>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    k_gemm_b(int Mfix, int N, int Kfix, const int32_t* const* dM, const int32_t* const* dK,
+             Act<T> A, Act<T> B, Act<T> C, int accumulate) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  const int z = blockIdx.z;
+  const int M = dM ? *dM[z] : Mfix;
+  const int K = dK ? *dK[z] : Kfix;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   if (m0 >= M) return;
-  __shared__ T As[GBK][GBM + 4];
-  __shared__ T Bs[GBK][GBN + 4];
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  T acc[4][4];
+  const T* __restrict__ a = A.at(z);
+  const T* __restrict__ b = B.at(z);
+  T* __restrict__ c = C.at(z);
+  __shared__ T As[BK][BM + 4];
+  __shared__ T Bs[BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  T acc[TM][TN];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < TM; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = T(0);
-  for (int k0 = 0; k0 < K; k0 += GBK) {
+    for (int j = 0; j < TN; ++j) acc[i][j] = T(0);
+  for (int k0 = 0; k0 < K; k0 += BK) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int idx = tid + q * 256;
+    for (int q = 0; q < (BM * BK) / NT; ++q) {
+      const int idx = tid + q * NT;
       int m, k;
-      if (TA) { k = idx / GBM; m = idx % GBM; } else { m = idx / GBK; k = idx % GBK; }
+      if (TA) { k = idx / BM; m = idx % BM; } else { m = idx / BK; k = idx % BK; }
       const int gm = m0 + m, gk = k0 + k;
       T v = T(0);
-      if (gm < M && gk < K) v = TA ? A[(int64_t)gk * lda + gm] : A[(int64_t)gm * lda + gk];
+      if (gm < M && gk < K) v = TA ? a[(int64_t)gk * A.ld + gm] : a[(int64_t)gm * A.ld + gk];
       As[k][m] = v;
-      int n, kb;
-      if (TB) { n = idx / GBK; kb = idx % GBK; } else { kb = idx / GBN; n = idx % GBN; }
-      const int gn = n0 + n, gkb = k0 + kb;
-      T u = T(0);
-      if (gn < N && gkb < K) u = TB ? B[(int64_t)gn * ldb + gkb] : B[(int64_t)gkb * ldb + gn];
-      Bs[kb][n] = u;
+    }
+#pragma unroll
+    for (int q = 0; q < (BN * BK) / NT; ++q) {
+      const int idx = tid + q * NT;
+      int n, k;
+      if (TB) { n = idx / BK; k = idx % BK; } else { k = idx / BN; n = idx % BN; }
+      const int gn = n0 + n, gk = k0 + k;
+      T v = T(0);
+      if (gn < N && gk < K) v = TB ? b[(int64_t)gn * B.ld + gk] : b[(int64_t)gk * B.ld + gn];
+      Bs[k][n] = v;
     }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < GBK; ++kk) {
-      T a[4], b[4];
+    for (int kk = 0; kk < BK; ++kk) {
+      T av[TM], bv[TN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+      for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+      for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < TN; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int gm = m0 + ty * 4 + i;
+  for (int i = 0; i < TM; ++i) {
+    const int gm = m0 + ty * TM + i;
     if (gm >= M) continue;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int gn = n0 + tx * 4 + j;
+    for (int j = 0; j < TN; ++j) {
+      const int gn = n0 + tx * TN + j;
       if (gn >= N) continue;
-      T* c = C + (int64_t)gm * ldc + gn;
-      *c = accumulate ? *c + acc[i][j] : acc[i][j];
+      T* p = c + (int64_t)gm * C.ld + gn;
+      *p = accumulate ? *p + acc[i][j] : acc[i][j];
     }
   }
 }
 
+template <typename T, int BM, int BN, int BK, int TM, int TN>
+static void gemm_launch(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+                        const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool acc,
+                        cudaStream_t st) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, n);
+  if (!ta && !tb) GLAUNCH((k_gemm_b<T, false, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  else if (ta && !tb) GLAUNCH((k_gemm_b<T, true, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  else if (!ta && tb) GLAUNCH((k_gemm_b<T, false, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  else GLAUNCH((k_gemm_b<T, true, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+}
+
 template <typename T>
-void gemm(bool ta, bool tb, int M, int N, int K, const int32_t* dM, const int32_t* dK, const T* A,
-          int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool accumulate,
-          cudaStream_t st) {
-  if (M <= 0 || N <= 0) return;
-  dim3 grid((N + GBN - 1) / GBN, (M + GBM - 1) / GBM);
-  if (!ta && !tb) GLAUNCH((k_gemm<T, false, false><<<grid, 256, 0, st>>>(M, N, K, dM, dK, A, lda, B, ldb, C, ldc, accumulate)));
-  else if (ta && !tb) GLAUNCH((k_gemm<T, true, false><<<grid, 256, 0, st>>>(M, N, K, dM, dK, A, lda, B, ldb, C, ldc, accumulate)));
-  else if (!ta && tb) GLAUNCH((k_gemm<T, false, true><<<grid, 256, 0, st>>>(M, N, K, dM, dK, A, lda, B, ldb, C, ldc, accumulate)));
-  else GLAUNCH((k_gemm<T, true, true><<<grid, 256, 0, st>>>(M, N, K, dM, dK, A, lda, B, ldb, C, ldc, accumulate)));
+void gemm_b(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+            const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool accumulate,
+            cudaStream_t st) {
+  if (M <= 0 || N <= 0 || n <= 0) return;
+  if (sizeof(T) == 4 && N > 32)
+    gemm_launch<T, 128, 64, 16, 8, 4>(ta, tb, n, M, N, K, dM, dK, A, B, C, accumulate, st);
+  else
+    gemm_launch<T, 64, 64, 16, 4, 4>(ta, tb, n, M, N, K, dM, dK, A, B, C, accumulate, st);
+}
+
+template <typename T>
+void gemm_plain(int M, int N, int K, const T* A, int64_t lda, const T* B, int64_t ldb, T* C,
+                int64_t ldc, cudaStream_t st) {
+  Act<T> a{const_cast<T*>(A), 0, lda}, b{const_cast<T*>(B), 0, ldb}, c{C, 0, ldc};
+  gemm_b<T>(false, false, 1, M, N, K, nullptr, nullptr, a, b, c, false, st);
+}
+
+// deterministic split-K reduction: C (+)= P_0 + P_1 + ... in slot order
+template <typename T>
+__global__ void k_reduce_slots(const T* parts, int64_t pstride, int n, int64_t rows, int64_t cols,
+                               int64_t ldp, T* C, int64_t ldc, int accumulate) {
+  const int64_t total = rows * cols;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i % cols;
+    T s = accumulate ? C[r * ldc + c] : T(0);
+    for (int z = 0; z < n; ++z) s += parts[z * pstride + r * ldp + c];
+    C[r * ldc + c] = s;
+  }
+}
+
+template <typename T>
+void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int64_t cols,
+                  int64_t ldp, T* C, int64_t ldc, bool accumulate, cudaStream_t st) {
+  int64_t total = rows * cols;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * sms());
+  GLAUNCH((k_reduce_slots<T><<<std::max(blocks, 1), 256, 0, st>>>(parts, part_stride, n, rows, cols,
+                                                                 ldp, C, ldc, accumulate)));
 }
 
 // ------------------------------------------------------------------ softmax CE (K11)
-// training.py:293-308: LSE loss averaged over labelled batch rows and its gradient.
+// training.py:293-308: per-row LSE loss and gradient (warp per row, all slots), then a
+// fixed-order per-slot mean.
 template <typename T>
-__global__ void k_softmax_ce(const int32_t* d_rows, const int32_t* batch, const int32_t* labels,
-                             const T* Z, int64_t ldz, int C, T* G, int64_t ldg, double* loss_out,
-                             int32_t* err) {
-  const int n = *d_rows;
+__global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T> Z, int C,
+                               Act<T> G, double* row_loss, int64_t rl_stride) {
+  const SlotDesc d = sd[blockIdx.y];
+  const int n = *d.n_batch;
   __shared__ int s_nlab;
-  __shared__ double wsum[32];
-  typedef cub::BlockReduce<int, 1024> BR;
+  typedef cub::BlockReduce<int, 256> BR;
   __shared__ typename BR::TempStorage tmp;
-  int c = 0;
-  for (int r = threadIdx.x; r < n; r += blockDim.x) c += labels[batch[r]] >= 0;
-  int tot = BR(tmp).Sum(c);
+  int cnt = 0;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) cnt += labels[d.batch[r]] >= 0;
+  int tot = BR(tmp).Sum(cnt);
   if (threadIdx.x == 0) s_nlab = tot;
   __syncthreads();
   const int nlab = s_nlab;
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double part = 0.0;
-  for (int r = w; r < n; r += 32) {
-    const int y = labels[batch[r]];
-    T* g = G + (int64_t)r * ldg;
+  const T* z0 = Z.at(blockIdx.y);
+  T* g0 = G.at(blockIdx.y);
+  double* rl = row_loss + blockIdx.y * rl_stride;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int y = labels[d.batch[r]];
+    T* g = g0 + (int64_t)r * G.ld;
     if (y < 0 || nlab == 0) {
       for (int k = lane; k < C; k += 32) g[k] = T(0);
+      if (lane == 0) rl[r] = 0.0;
       continue;
     }
-    const T* z = Z + (int64_t)r * ldz;
+    const T* z = z0 + (int64_t)r * Z.ld;
     double zmax = -INFINITY;
     for (int k = lane; k < C; k += 32) zmax = fmax(zmax, (double)z[k]);
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) zmax = fmax(zmax, __shfl_xor_sync(FULLM, zmax, d));
+    for (int o = 16; o > 0; o >>= 1) zmax = fmax(zmax, __shfl_xor_sync(FULLM, zmax, o));
     double se = 0.0;
     for (int k = lane; k < C; k += 32) se += exp((double)z[k] - zmax);
 #pragma unroll
-    for (int d = 16; d > 0; d >>= 1) se += __shfl_xor_sync(FULLM, se, d);
+    for (int o = 16; o > 0; o >>= 1) se += __shfl_xor_sync(FULLM, se, o);
     const double lse = zmax + log(se);
     for (int k = lane; k < C; k += 32) {
       double gz = exp((double)z[k] - lse) - (k == y ? 1.0 : 0.0);
       g[k] = (T)(gz / nlab);
     }
-    if (lane == 0) part += lse - (double)z[y];
+    if (lane == 0) rl[r] = lse - (double)z[y];
   }
-  if (lane == 0) wsum[w] = part;
-  __syncthreads();
+}
+
+__global__ void k_loss_mean(const SlotDesc* sd, const int32_t* labels, const double* row_loss,
+                            int64_t rl_stride, double* loss_out) {
+  const SlotDesc d = sd[blockIdx.x];
+  const int n = *d.n_batch;
+  typedef cub::BlockReduce<double, 256> BRD;
+  typedef cub::BlockReduce<int, 256> BRI;
+  __shared__ typename BRD::TempStorage td;
+  __shared__ typename BRI::TempStorage ti;
+  double s = 0.0;
+  int c = 0;
+  const double* rl = row_loss + blockIdx.x * rl_stride;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) {  // fixed assignment: deterministic
+    if (labels[d.batch[r]] >= 0) {
+      s += rl[r];
+      ++c;
+    }
+  }
+  double tot = BRD(td).Sum(s);
+  int cnt = BRI(ti).Sum(c);
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < 32; ++i) s += wsum[i];
-    *loss_out = nlab ? s / nlab : __longlong_as_double(0x7ff8000000000000LL);
-    if (!nlab) atomicOr(err, EB_NO_LABELS);
+    loss_out[blockIdx.x] = cnt ? tot / cnt : __longlong_as_double(0x7ff8000000000000LL);
+    if (!cnt) atomicOr(d.err, EB_NO_LABELS);
   }
 }
 
 template <typename T>
-void softmax_ce(const int32_t* d_rows, int max_rows, const int32_t* batch, const int32_t* labels,
-                const T* logits, int64_t ldz, int C, T* grad, int64_t ldg, double* loss_out,
-                int32_t* err, cudaStream_t st) {
-  GLAUNCH((k_softmax_ce<T><<<1, 1024, 0, st>>>(d_rows, batch, labels, logits, ldz, C, grad, ldg,
-                                               loss_out, err)));
+void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
+                  Act<T> G, double* row_loss, double* loss_out, cudaStream_t st) {
+  GLAUNCH((k_softmax_ce_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(
+      sd, labels, Z, C, G, row_loss, max_rows)));
+  GLAUNCH((k_loss_mean<<<n, 256, 0, st>>>(sd, labels, row_loss, max_rows, loss_out)));
 }
 
 // ------------------------------------------------------------------ optimizers (K12 epilogue)
@@ -369,23 +441,23 @@ void fill_zero(T* p, int64_t n, cudaStream_t st) {
   GLAUNCH(k_zero<T><<<std::max(blocks, 1), 256, 0, st>>>(p, n));
 }
 
-#define INST(T)                                                                                      \
-  template void gather_rows<T>(const FeatStore&, const int32_t*, const int32_t*, int, T*, int64_t,   \
-                               cudaStream_t);                                                        \
-  template void spmm<T>(const int32_t*, int, const int32_t*, const int32_t*, const double*, const T*, \
-                        int64_t, bool, T*, int64_t, int64_t, cudaStream_t);                          \
-  template void spmm_t_mask<T>(const int32_t*, int, const int32_t*, const int32_t*, const double*,   \
-                               const T*, int64_t, const T*, int64_t, T*, int64_t, int64_t,           \
-                               cudaStream_t);                                                        \
-  template void gemm<T>(bool, bool, int, int, int, const int32_t*, const int32_t*, const T*, int64_t, \
-                        const T*, int64_t, T*, int64_t, bool, cudaStream_t);                         \
-  template void softmax_ce<T>(const int32_t*, int, const int32_t*, const int32_t*, const T*, int64_t, \
-                              int, T*, int64_t, double*, int32_t*, cudaStream_t);                    \
-  template void sgd_step<T>(T*, const T*, int64_t, double, double, cudaStream_t);                    \
-  template void adam_step<T>(T*, const T*, T*, T*, int64_t, double, double, double, double, double,  \
-                             double, double, double, double, cudaStream_t);                          \
-  template void spmm_full<T>(int64_t, const int64_t*, const int32_t*, const double*, const T*,       \
-                             int64_t, bool, T*, int64_t, int64_t, cudaStream_t);                     \
+#define INST(T)                                                                                     \
+  template void gather_rows_b<T>(const FeatStore&, const SlotDesc*, int, int, Act<T>, cudaStream_t); \
+  template void spmm_b<T>(const LayerDesc*, int, int, bool, bool, Act<T>, Act<T>, Act<T>, int64_t,  \
+                          cudaStream_t);                                                            \
+  template void gemm_b<T>(bool, bool, int, int, int, int, const int32_t* const*,                    \
+                          const int32_t* const*, Act<T>, Act<T>, Act<T>, bool, cudaStream_t);       \
+  template void reduce_slots<T>(const T*, int64_t, int, int64_t, int64_t, int64_t, T*, int64_t,     \
+                                bool, cudaStream_t);                                                \
+  template void softmax_ce_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>,     \
+                                double*, double*, cudaStream_t);                                    \
+  template void sgd_step<T>(T*, const T*, int64_t, double, double, cudaStream_t);                   \
+  template void adam_step<T>(T*, const T*, T*, T*, int64_t, double, double, double, double, double, \
+                             double, double, double, double, cudaStream_t);                         \
+  template void spmm_full<T>(int64_t, const int64_t*, const int32_t*, const double*, const T*,      \
+                             int64_t, bool, T*, int64_t, int64_t, cudaStream_t);                    \
+  template void gemm_plain<T>(int, int, int, const T*, int64_t, const T*, int64_t, T*, int64_t,     \
+                              cudaStream_t);                                                        \
   template void fill_zero<T>(T*, int64_t, cudaStream_t);
 INST(float)
 INST(double)

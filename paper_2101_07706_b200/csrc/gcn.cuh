@@ -1,4 +1,5 @@
-// GCN forward/backward kernels over a sampled plan (training.py:261-318).
+// GCN forward/backward kernels over sampled plans (training.py:261-318), batched over
+// the plans (slots) of an iteration: every stage is one launch with the slot on a grid axis.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -17,26 +18,53 @@ struct FeatStore {
   int64_t dim;                // true feature dimension
 };
 
+// Block of bottom-up layer l of one slot (device pointers into the plan arena).
+struct LayerDesc {
+  const int32_t* rows;  // |S_{l+1}| (device scalar)
+  const int32_t* cols;  // |S_l|     (device scalar)
+  const int32_t* indptr;
+  const int32_t* indices;
+  const double* val;
+  const int32_t* tindptr;
+  const int32_t* tindices;
+  const double* tval;
+};
+
+struct SlotDesc {
+  const int32_t* in_nodes;  // S_0 ids
+  const int32_t* n_in;      // |S_0|
+  const int32_t* batch;     // output rows' node ids (loss labels)
+  const int32_t* n_batch;   // rows of the logits
+  int32_t* err;
+};
+
+// Strided view of one activation buffer: slot z at base + z*stride, rows of ld elements.
 template <typename T>
-void gather_rows(const FeatStore& fs, const int32_t* ids, const int32_t* d_n, int max_n, T* out,
-                 int64_t ldo, cudaStream_t st);
+struct Act {
+  T* base;
+  int64_t stride, ld;
+  __host__ __device__ T* at(int z) const { return base + (int64_t)z * stride; }
+};
+
 template <typename T>
-void spmm(const int32_t* d_rows, int max_rows, const int32_t* indptr, const int32_t* indices,
-          const double* val, const T* A, int64_t lda, bool relu_in, T* out, int64_t ldo,
-          int64_t width, cudaStream_t st);
+void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows, Act<T> out,
+                   cudaStream_t st);
+// out = Block_l (relu?(A))  or, transposed, out = (Block_l^T A) * [H > 0]
 template <typename T>
-void spmm_t_mask(const int32_t* d_rows, int max_rows, const int32_t* indptr,
-                 const int32_t* indices, const double* val, const T* G, int64_t ldg,
-                 const T* H, int64_t ldh, T* out, int64_t ldo, int64_t width, cudaStream_t st);
-// C = op(A) op(B) (+ C if accumulate).  M or K may be read from device (dM / dK non-null).
+void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
+            Act<T> H, Act<T> out, int64_t width, cudaStream_t st);
+// C_z = op(A_z) op(B_z) (+ C_z).  M (or K) per slot from device scalars rows[z] when given.
 template <typename T>
-void gemm(bool ta, bool tb, int M, int N, int K, const int32_t* dM, const int32_t* dK,
-          const T* A, int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, bool accumulate,
-          cudaStream_t st);
+void gemm_b(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+            const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool accumulate,
+            cudaStream_t st);
+// C (+)= sum_z P_z in slot order (deterministic split-K reduction)
 template <typename T>
-void softmax_ce(const int32_t* d_rows, int max_rows, const int32_t* batch, const int32_t* labels,
-                const T* logits, int64_t ldz, int C, T* grad, int64_t ldg, double* loss_out,
-                int32_t* err, cudaStream_t st);
+void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int64_t cols,
+                  int64_t ldp, T* C, int64_t ldc, bool accumulate, cudaStream_t st);
+template <typename T>
+void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
+                  Act<T> G, double* row_loss, double* loss_out, cudaStream_t st);
 template <typename T>
 void sgd_step(T* w, const T* g, int64_t n, double lr, double contrib, cudaStream_t st);
 template <typename T>
@@ -46,6 +74,9 @@ void adam_step(T* w, const T* g, T* m, T* v, int64_t n, double lr, double contri
 template <typename T>
 void spmm_full(int64_t n, const int64_t* off, const int32_t* col, const double* w, const T* A,
                int64_t lda, bool relu_in, T* out, int64_t ldo, int64_t width, cudaStream_t st);
+template <typename T>
+void gemm_plain(int M, int N, int K, const T* A, int64_t lda, const T* B, int64_t ldb, T* C,
+                int64_t ldc, cudaStream_t st);
 template <typename T>
 void fill_zero(T* p, int64_t n, cudaStream_t st);
 

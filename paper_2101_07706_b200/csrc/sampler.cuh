@@ -69,6 +69,7 @@ struct PlanDev {
   int32_t* word_prefix;     // [n_words]
   int64_t* tile_a;          // [cap_tiles]
   int64_t* tile_b;          // [cap_tiles]
+  int64_t* tile_c;          // [cap_tiles]
   int32_t* bucket_off;      // [cap_cand+1]
   int32_t* bucket_r;        // [cap_pairs]
   double* bucket_w;         // [cap_pairs]
@@ -107,7 +108,7 @@ struct PlanDev {
   LayerStat* stat;          // [L]
 };
 
-constexpr int kTileWords = 4096;   // bitmap words per compaction tile (1024 threads x 4)
+constexpr int kTileWords = 256;    // bitmap words per compaction tile (8 warps x 32 words)
 constexpr int kTileCand = 4096;    // candidates per scan tile
 constexpr int kSmallBucket = 16;   // buckets folded in registers
 constexpr int kChunk = 32;         // exact-cumsum chunk (one warp)

@@ -538,10 +538,13 @@ class Trainer:
                                        ptr(self._states, C.c_uint64), self.stream))
 
     def compute(self, epoch, it):
-        check(lib.skg_zero(self.dtc, self.gflat.data_ptr(), self.n_params, self.stream))
-        for i in range(len(self.mine)):
-            check(lib.skg_gcn_step(self.gcn, i, ptr(self.wp, C.c_uint64), ptr(self.gp, C.c_uint64), 1,
-                                   self.losses[it % self.per_epoch, i].data_ptr(), self.stream))
+        if self.mine:
+            # all of this rank's workers in one batched pass; gradients summed in worker order
+            check(lib.skg_gcn_step_batch(self.gcn, 0, len(self.mine), ptr(self.wp, C.c_uint64),
+                                         ptr(self.gp, C.c_uint64), 0,
+                                         self.losses[it % self.per_epoch].data_ptr(), self.stream))
+        else:
+            check(lib.skg_zero(self.dtc, self.gflat.data_ptr(), self.n_params, self.stream))
         if self.mine:
             check(lib.skg_plans_ledger_add(self.ps.h, len(self.mine),
                                            self.ledger[epoch % self.ledger.shape[0]].data_ptr(),
