@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--lr", type=float, default=0.5)
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-stages", action="store_true", default=True)
+    ap.add_argument("--ahead", type=int, default=4, help="iterations of plans per sampler launch")
     return ap.parse_args()
 
 
@@ -159,51 +159,59 @@ def run_ours(args):
     model = P.init_model(dims, seed=0)
     cfg = P.SamplerConfig(budget=args.budget, skew_constant=args.D, mode=args.mode)
     P.set_compute_dtype(args.dtype)
+    T = max(1, args.ahead)
     tr = P.Trainer(g, part, model, cfg, batch_size=args.batch, lr=args.lr, mode=args.mode,
-                   seed=0, dtype=args.dtype, epochs=1)
+                   seed=0, dtype=args.dtype, epochs=1, ahead=T)
     stream = torch.cuda.current_stream()
-    n_my = len(tr.mine)
-    W, K = args.warmup, args.steps
+    n_my = tr.n_my
+    W = max(args.warmup, 1)
+    K = ((args.steps + T - 1) // T) * T          # whole look-ahead groups
+    W = ((W + T - 1) // T) * T
     per = tr.per_epoch
 
-    # ---- inputs resident in HBM: batch ids + plan states for every step, derived up front
+    # ---- inputs resident in HBM: batch ids + plan states of every step, derived up front
     total_steps = W + K
     bl = np.zeros((total_steps, n_my), dtype=np.int32)
     states = np.zeros((total_steps, n_my, 4), dtype=np.uint64)
     ids = np.zeros((total_steps, n_my, args.batch), dtype=np.int32)
     for s in range(total_steps):
-        boff, bids, st = tr.host_inputs(s // per, s % per)
+        boff, bids, st = tr.host_inputs(s // per, s % per, 0)
         for i in range(n_my):
             n_i = boff[i + 1] - boff[i]
             bl[s, i] = n_i
             ids[s, i, :n_i] = bids[boff[i]:boff[i + 1]]
         states[s] = st[:n_my]
     d_ids = torch.as_tensor(ids, device="cuda")
-    workers = np.array(tr.mine, dtype=np.int32)
+    workers = np.array(tr.mine * T, dtype=np.int32)
 
-    def step_resident(s):
+    def sample_resident(s0, n):
         check(lib.skg_ladies_sample_device(
-            tr.ps.h, n_my, ptr(workers, C.c_int32), ptr(np.ascontiguousarray(bl[s]), C.c_int32),
-            d_ids[s].data_ptr(), args.batch, MODES[args.mode], float(args.D), 1.0,
-            ptr(np.ascontiguousarray(states[s]), C.c_uint64), tr.stream))
-        tr.compute(0, s % per)
-        tr.reduce_and_step()
+            tr.ps.h, n * n_my, ptr(workers, C.c_int32),
+            ptr(np.ascontiguousarray(bl[s0:s0 + n].reshape(-1)), C.c_int32),
+            d_ids[s0].data_ptr(), args.batch, MODES[args.mode], float(args.D), 1.0,
+            ptr(np.ascontiguousarray(states[s0:s0 + n].reshape(-1, 4)), C.c_uint64), tr.stream))
+
+    def steps_resident(s0, count):
+        for g0 in range(s0, s0 + count, T):
+            n = min(T, s0 + count - g0)
+            sample_resident(g0, n)
+            for gi in range(n):
+                tr.compute(0, (g0 + gi) % per, gi)
+                tr.reduce_and_step()
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    for s in range(W):
-        step_resident(s)
+    steps_resident(0, W)
     barrier()
     launches0 = P.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
-        for s in range(W, W + K):
-            step_resident(s)
+        steps_resident(W, K)
         ev1.record(stream)
         barrier()
     launches = P.kernel_launches() - launches0
@@ -215,33 +223,29 @@ def run_ours(args):
     tr.check_errors()
     ms_per_step = ms / K
 
-    # ---- ledger and per-stage split on one more (instrumented) pass
+    # ---- ledger, plan statistics and the per-stage split (separate instrumented pass)
     ledger = tr.ledger[0].clone()
     if dist is not None:
         dist.all_reduce(ledger)
     remote_per_iter = float(ledger.sum().item()) / (W + K)
-    stats = [tr.ps.stats(i)[0] for i in range(n_my)]
-    s0_remote = sum(int(st[N_LAYERS - 1, 4]) for st in stats)  # input-layer remote rows (moved)
-    sampled_nodes = sum(int(st[:, 2].sum()) for st in stats)
-    alg_bytes = sum(algorithmic_sampler_bytes(st) for st in stats)
-
-    e_s = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    stats = [tr.ps.stats(i)[0] for i in range(n_my * T)]
+    s0_remote = sum(int(st[N_LAYERS - 1, 4]) for st in stats) / T   # input-layer rows moved
+    sampled_nodes = sum(int(st[:, 2].sum()) for st in stats) / T
+    alg_bytes = sum(algorithmic_sampler_bytes(st) for st in stats)   # one T-plan launch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
     samp_ms, comp_ms = [], []
-    for rep in range(5):
-        s = W + (rep % K)
-        e_s[0].record(stream)
-        check(lib.skg_ladies_sample_device(
-            tr.ps.h, n_my, ptr(workers, C.c_int32), ptr(np.ascontiguousarray(bl[s]), C.c_int32),
-            d_ids[s].data_ptr(), args.batch, MODES[args.mode], float(args.D), 1.0,
-            ptr(np.ascontiguousarray(states[s]), C.c_uint64), tr.stream))
-        e_s[1].record(stream)
-        tr.compute(0, s % per)
-        e_s[2].record(stream)
-        tr.reduce_and_step()
-        e_s[3].record(stream)
+    for rep in range(3):
+        s0 = W + (rep * T) % K
+        ev[0].record(stream)
+        sample_resident(s0, T)
+        ev[1].record(stream)
+        for gi in range(T):
+            tr.compute(0, (s0 + gi) % per, gi)
+            tr.reduce_and_step()
+        ev[2].record(stream)
         torch.cuda.synchronize()
-        samp_ms.append(e_s[0].elapsed_time(e_s[1]))
-        comp_ms.append(e_s[1].elapsed_time(e_s[2]))
+        samp_ms.append(ev[0].elapsed_time(ev[1]))
+        comp_ms.append(ev[1].elapsed_time(ev[2]) / T)
     samp = float(np.median(samp_ms))
     peaks = {}
     try:
@@ -252,19 +256,16 @@ def run_ours(args):
     achieved = alg_bytes / (samp * 1e-3) / 1e9
 
     # ---- e2e through the public API: host-derived inputs, H2D each step, loss D2H
-    ev2, ev3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    h2d = 0
     barrier()
+    h2d = [0]
+
+    def read_loss(e, it):
+        h2d[0] += int(tr._boff[n_my]) * 4 + n_my * 32
+        _ = tr.losses[it % per].cpu()  # the step's result to host
+
+    pairs = [(s // per, s % per) for s in range(K)]
     t_e2e0 = time.perf_counter()
-    ev2.record(stream)
-    for s in range(K):
-        boff, bids, _ = tr.host_inputs(s // per, s % per)
-        h2d += int(boff[n_my]) * 4 + n_my * 32
-        tr.sample()
-        tr.compute(0, s % per)
-        tr.reduce_and_step()
-        _ = tr.losses[s % per].cpu()  # step result to host
-    ev3.record(stream)
+    tr.run(pairs, on_iteration=read_loss)
     barrier()
     e2e_ms = (time.perf_counter() - t_e2e0) * 1e3
     if dist is not None:
@@ -294,19 +295,21 @@ def run_ours(args):
                                    f"workers, batch {args.batch}, budget {args.budget}, "
                                    f"{N_LAYERS} layers hidden {DIMS_HIDDEN}",
                        "n_nodes": sg.n_nodes, "nnz": sg.nnz, "workers": k,
+                       "plans_per_sampler_launch": T * n_my, "lookahead_iters": T,
                        "l2": "inputs > L2 (114M-entry CSR, 561 MB features); no flush"},
             "remote_nodes_per_iter": round(remote_per_iter, 2),
             "input_layer_remote_rows_per_iter": s0_remote,
             "sampled_nodes_per_s": round(sampled_nodes / (ms_per_step * 1e-3), 1),
             "gpu_launches": int(launches),
-            "stages_ms": {"sample": round(samp, 4), "gcn_fwd_bwd": round(float(np.median(comp_ms)), 4)},
-            "roofline": {"bound": "hbm", "kernel": "sampler (LADIES, all layers, one batched launch "
-                                                     "sequence)",
+            "stages_ms_per_iter": {"sample": round(samp / T, 4),
+                                   "gcn_fwd_bwd_step": round(float(np.median(comp_ms)), 4)},
+            "roofline": {"bound": "hbm", "kernel": f"sampler (LADIES, 5 layers x {T * n_my} plans, "
+                                                     "one batched launch sequence)",
                          "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
                          "frac": round(achieved / hbm, 5), "traffic": None,
-                         "algorithmic_bytes": int(alg_bytes)},
+                         "algorithmic_bytes": int(alg_bytes), "duration_ms": round(samp, 4)},
             "e2e": {"value": round(1000.0 * K / e2e_ms, 3), "unit": "iters/s",
-                    "h2d_bytes_per_step": int(h2d // K), "d2h_bytes_per_step": 8 * n_my},
+                    "h2d_bytes_per_step": int(h2d[0] // K), "d2h_bytes_per_step": 8 * n_my},
             "clocks": clk.summary(),
             "graph_build_s": round(t_gen, 2),
         }

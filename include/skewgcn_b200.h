@@ -115,8 +115,8 @@ int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, int mode,
                      double skew_constant, double min_scale, const uint64_t* rng_states,
                      void* stream);
 /* CommLedger.add_plan (training.py:127-128) on device: ledger_dev is int64 [k x n_layers]
- * (one epoch); adds remote_per_layer of slots [0, n) to the rows of their workers. */
-int skg_plans_ledger_add(skg_plans* ps, int n, uint64_t ledger_dev, void* stream);
+ * (one epoch); adds remote_per_layer of slots [slot0, slot0+n) to their workers' rows. */
+int skg_plans_ledger_add(skg_plans* ps, int slot0, int n, uint64_t ledger_dev, void* stream);
 /* Synchronous readback.  stats: n_layers x 16 int64 (doubles bit-cast):
  * [n_upper, n_cand, n_nodes, nnz, remote, has_dist, n_remote_cand, starved, skew,
  *  n_pairs, kept_pairs, s, total, T, pw_depth, 0]; info: [err_bits, draws_consumed,

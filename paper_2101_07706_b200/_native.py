@@ -54,7 +54,7 @@ _sig("skg_ctx_feature_ptr", C.c_int, vp, P(u64), P(i64))
 _sig("skg_ctx_set_labels", C.c_int, vp, P(i64))
 _sig("skg_ctx_info", C.c_int, vp, P(i64))
 _sig("skg_ctx_set_owner", C.c_int, vp, i32, P(i32))
-_sig("skg_plans_ledger_add", C.c_int, vp, C.c_int, u64, vp)
+_sig("skg_plans_ledger_add", C.c_int, vp, C.c_int, C.c_int, u64, vp)
 _sig("skg_ipc_handle", C.c_int, u64, P(C.c_uint8))
 _sig("skg_ipc_open", C.c_int, P(C.c_uint8), P(u64))
 _sig("skg_ipc_close", C.c_int, u64)

@@ -524,6 +524,7 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     cv.add(P.super_mode, cap_supers);
     cv.add(P.super_start, cap_supers);
     cv.add(P.cdf, cap_cand);
+    cv.add(P.qarr, cap_cand);
     cv.add(P.draw_idx, budget);
     cv.add(P.cand, kind == KIND_LADIES ? (size_t)Ls * cap_cand : 1);
     cv.add(P.norm, (size_t)Ls * cap_cand);
@@ -808,9 +809,10 @@ __global__ void k_ledger_add(const PlanDev* plans, int L, int64_t* ledger) {
   }
 }
 
-extern "C" int skg_plans_ledger_add(skg_plans* ps, int n, uint64_t ledger_dev, void* stream) {
-  ARG(ps && n >= 1 && n <= ps->n_slots && ledger_dev, "bad ledger arguments");
-  k_ledger_add<<<n, 32, 0, (cudaStream_t)stream>>>(ps->d_plans, ps->L, (int64_t*)ledger_dev);
+extern "C" int skg_plans_ledger_add(skg_plans* ps, int slot0, int n, uint64_t ledger_dev,
+                                    void* stream) {
+  ARG(ps && slot0 >= 0 && n >= 1 && slot0 + n <= ps->n_slots && ledger_dev, "bad ledger arguments");
+  k_ledger_add<<<n, 32, 0, (cudaStream_t)stream>>>(ps->d_plans + slot0, ps->L, (int64_t*)ledger_dev);
   ++g_kernel_launches;
   CK(cudaGetLastError());
   return SKG_OK;

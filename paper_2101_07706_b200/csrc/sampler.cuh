@@ -88,6 +88,7 @@ struct PlanDev {
   int32_t* super_mode;      // [cap_supers]
   double* super_start;      // [cap_supers]
   double* cdf;              // [cap_cand]
+  double* qarr;             // [cap_cand] q of the layer being sampled
   int32_t* draw_idx;        // [budget]
   int64_t* draws_consumed;  // [1] uniforms consumed by this plan so far
   int32_t* err;             // [1] ErrBits

@@ -422,11 +422,17 @@ def assign_workers(active, rank: int, world: int):
 
 
 class Trainer:
-    """Device-resident training state for ``train_distributed`` (and the benchmark)."""
+    """Device-resident training state for ``train_distributed`` (and the benchmark).
+
+    Plans depend only on (seed, epoch, iteration, worker), never on the weights
+    (training.py:488-493), so the plans of ``ahead`` future iterations are sampled by one
+    batched launch sequence (``sample_group``) and consumed one iteration at a time by
+    ``compute`` + ``reduce_and_step``; results are identical to sampling them one by one.
+    """
 
     def __init__(self, g, partition, model, cfg, *, batch_size, lr, mode, seed,
                  sampler="ladies", subgraph_size=None, optimizer="sgd", dtype=None,
-                 epochs=1, workers=None):
+                 epochs=1, workers=None, ahead=1):
         torch = _torch()
         if g.features is None or g.labels is None or g.train_mask is None:
             raise ValueError("training needs features, labels and masks")
@@ -465,11 +471,13 @@ class Trainer:
         self.subgraph_size = subgraph_size
         self.dist, self.rank, self.world = _dist_info()
         self.mine = workers if workers is not None else assign_workers(self.active, self.rank, self.world)
+        self.n_my = len(self.mine)
+        self.ahead = max(1, int(ahead))
         self.dg = D.device_graph(g)
         self.dg.ensure_owner(partition)
         self.dg.ensure_features(g.features, self.dtype)
         self.dg.ensure_labels(np.asarray(g.labels))
-        n_slots = max(1, len(self.mine))
+        n_slots = max(1, self.n_my * self.ahead)
         if sampler == "ladies":
             self.ps = self.dg.acquire(KIND_LADIES, n_slots, self.L, int(self.cfg.budget), int(batch_size))
         else:
@@ -496,36 +504,51 @@ class Trainer:
             self.t = 0
         self.epochs = epochs
         self.ledger = torch.zeros((max(epochs, 1), self.k, self.L), dtype=torch.int64, device="cuda")
-        self.losses = torch.zeros((self.per_epoch, max(1, len(self.mine))), dtype=torch.float64,
+        self.losses = torch.zeros((self.per_epoch, max(1, self.n_my)), dtype=torch.float64,
                                   device="cuda")
         self.stream = D.current_stream()
         self.dtc = DT[self.dtype]
-        self._workers = np.array(self.mine, dtype=np.int32)
-        self._states = np.zeros((max(1, len(self.mine)), 4), dtype=np.uint64)
-        self._boff = np.zeros(len(self.mine) + 1, dtype=np.int64)
-        self._bids = np.zeros(max(1, len(self.mine)) * max(1, batch_size), dtype=np.int64)
+        self._workers = np.array(self.mine * self.ahead, dtype=np.int32)
+        self._states = np.zeros((n_slots, 4), dtype=np.uint64)
+        self._boff = np.zeros(n_slots + 1, dtype=np.int64)
+        self._bids = np.zeros(n_slots * max(1, batch_size), dtype=np.int64)
         self._len = C.c_int64()
+        self._group = []  # (epoch, it) of the sampled-ahead slot groups
 
-    # -- one iteration (training.py:483-506) -------------------------------
-    def host_inputs(self, epoch, it):
-        """Batch ids and plan PCG64 states of this rank's workers (native host runtime)."""
-        o = 0
+    # -- host inputs / sampling -------------------------------------------
+    def host_inputs(self, epoch, it, group=0):
+        """Batch ids and plan PCG64 states of this rank's workers for one iteration,
+        into slot group ``group`` (native host runtime, training.py:488-493)."""
+        base = group * self.n_my
+        o = self._boff[base]
         for i, w in enumerate(self.mine):
+            s = base + i
             if self.sampler == "ladies":
                 tw = self.worker_train[w]
                 check(lib.skg_iteration_inputs(self.seed & 0xFFFFFFFFFFFFFFFF, epoch, it, w,
                                                ptr(tw, C.c_int64), len(tw), self.batch_size,
                                                ptr(self._bids[o:], C.c_int64), C.byref(self._len),
-                                               ptr(self._states[i], C.c_uint64)))
+                                               ptr(self._states[s], C.c_uint64)))
                 o += self._len.value
-                self._boff[i + 1] = o
+                self._boff[s + 1] = o
             else:
                 from .seeding import pcg64_state
-                self._states[i] = pcg64_state(self.seed, "plan", epoch, it, w)
+                self._states[s] = pcg64_state(self.seed, "plan", epoch, it, w)
         return self._boff, self._bids, self._states
 
-    def sample(self):
-        n = len(self.mine)
+    def sample_group(self, pairs):
+        """Sample the plans of iterations ``pairs`` = [(epoch, it), ...] in one launch."""
+        assert 1 <= len(pairs) <= self.ahead
+        self._boff[0] = 0
+        for gi, (e, it) in enumerate(pairs):
+            self.host_inputs(e, it, gi)
+        self._group = list(pairs)
+        self.sample(len(pairs) * self.n_my)
+
+    def sample(self, n=None):
+        n = self.n_my if n is None else n
+        if n == 0:
+            return
         if self.sampler == "ladies":
             check(lib.skg_ladies_sample(self.ps.h, n, ptr(self._workers, C.c_int32),
                                         ptr(self._boff, C.c_int64), ptr(self._bids, C.c_int64),
@@ -537,18 +560,19 @@ class Trainer:
                                        float(self.cfg.skew_constant), float(self.cfg.min_scale),
                                        ptr(self._states, C.c_uint64), self.stream))
 
-    def compute(self, epoch, it):
-        if self.mine:
+    # -- compute (training.py:499-506) --------------------------------------
+    def compute(self, epoch, it, group=0):
+        if self.n_my:
+            s0 = group * self.n_my
             # all of this rank's workers in one batched pass; gradients summed in worker order
-            check(lib.skg_gcn_step_batch(self.gcn, 0, len(self.mine), ptr(self.wp, C.c_uint64),
+            check(lib.skg_gcn_step_batch(self.gcn, s0, self.n_my, ptr(self.wp, C.c_uint64),
                                          ptr(self.gp, C.c_uint64), 0,
                                          self.losses[it % self.per_epoch].data_ptr(), self.stream))
-        else:
-            check(lib.skg_zero(self.dtc, self.gflat.data_ptr(), self.n_params, self.stream))
-        if self.mine:
-            check(lib.skg_plans_ledger_add(self.ps.h, len(self.mine),
+            check(lib.skg_plans_ledger_add(self.ps.h, s0, self.n_my,
                                            self.ledger[epoch % self.ledger.shape[0]].data_ptr(),
                                            self.stream))
+        else:
+            check(lib.skg_zero(self.dtc, self.gflat.data_ptr(), self.n_params, self.stream))
 
     def reduce_and_step(self):
         if self.world > 1:
@@ -564,13 +588,23 @@ class Trainer:
                                     float(self.lr), contrib, self.t, self.stream))
 
     def iteration(self, epoch, it):
-        self.host_inputs(epoch, it)
-        self.sample()
+        self.sample_group([(epoch, it)])
         self.compute(epoch, it)
         self.reduce_and_step()
 
+    def run(self, pairs, on_iteration=None):
+        """Train over iterations ``pairs`` in order, sampling ``ahead`` iterations at once."""
+        for g0 in range(0, len(pairs), self.ahead):
+            chunk = pairs[g0:g0 + self.ahead]
+            self.sample_group(chunk)
+            for gi, (e, it) in enumerate(chunk):
+                self.compute(e, it, gi)
+                self.reduce_and_step()
+                if on_iteration is not None:
+                    on_iteration(e, it)
+
     def check_errors(self):
-        for i in range(len(self.mine)):
+        for i in range(self.ps.n_slots):
             _, info, rc = self.ps.stats(i)
             check(rc)
 
@@ -585,52 +619,58 @@ class Trainer:
 def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, cfg: SamplerConfig, *,
                       epochs: int, batch_size: int, lr: float, mode: str, seed: int,
                       sampler: str = "ladies", subgraph_size: int | None = None,
-                      optimizer: str = "sgd") -> tuple:
+                      optimizer: str = "sgd", ahead: int = 4) -> tuple:
     """Data-parallel training with per-iteration gradient averaging (training.py:430-518).
 
     Single process: all workers run on this GPU.  Under torch.distributed (one process
     per GPU) each rank runs a contiguous block of workers and gradients are summed with
-    an NCCL all-reduce; metrics and ledger are identical on every rank.
+    an NCCL all-reduce; metrics and ledger are identical on every rank.  ``ahead``
+    iterations of plans are sampled per launch (plans never depend on the weights).
     """
     torch = _torch()
     tr = Trainer(g, partition, model, cfg, batch_size=batch_size, lr=lr, mode=mode, seed=seed,
-                 sampler=sampler, subgraph_size=subgraph_size, optimizer=optimizer, epochs=epochs)
+                 sampler=sampler, subgraph_size=subgraph_size, optimizer=optimizer, epochs=epochs,
+                 ahead=ahead)
     k, L = tr.k, tr.L
     metrics = Metrics()
     val_nodes = np.flatnonzero(g.val_mask) if g.val_mask is not None else np.empty(0, dtype=np.int64)
     labels_t = torch.as_tensor(np.asarray(g.labels), device="cuda")
+
+    def end_of_epoch(epoch, it):
+        if it != tr.per_epoch - 1:
+            return
+        losses = tr.losses.cpu().numpy()
+        ledger = tr.ledger[epoch]
+        loss_sum = np.zeros(k)
+        loss_cnt = np.zeros(k, dtype=np.int64)
+        for i, w in enumerate(tr.mine):  # python-float sums in iteration order
+            for j in range(tr.per_epoch):
+                loss_sum[w] += losses[j, i]
+                loss_cnt[w] += 1
+        if tr.world > 1:
+            ls = torch.as_tensor(loss_sum, device="cuda")
+            lc = torch.as_tensor(loss_cnt, device="cuda")
+            tr.dist.all_reduce(ls)
+            tr.dist.all_reduce(lc)
+            tr.dist.all_reduce(ledger)
+            loss_sum, loss_cnt = ls.cpu().numpy(), lc.cpu().numpy()
+        ledger_np = ledger.cpu().numpy()
+        logits = _predict_device(tr.dg, tr.wviews, tr.dims, tr.dtype)
+        preds = torch.argmax(logits, dim=1)
+        correct = (preds == labels_t).cpu().numpy()
+        val_acc = float(np.mean(correct[val_nodes])) if len(val_nodes) else 0.0
+        for w in range(k):
+            tw = tr.worker_train[w]
+            train_acc = float(np.mean(correct[tw])) if len(tw) else 0.0
+            mean_loss = float(loss_sum[w] / loss_cnt[w]) if loss_cnt[w] else 0.0
+            metrics.rows.append(MetricRow(epoch=epoch, worker=w, loss=mean_loss,
+                                          train_acc=train_acc, val_acc=val_acc,
+                                          comm_nodes_epoch=int(ledger_np[w].sum())))
+
     try:
-        for epoch in range(epochs):
-            for it in range(tr.per_epoch):
-                tr.iteration(epoch, it)
-            tr.check_errors()
-            losses = tr.losses.cpu().numpy()
-            ledger = tr.ledger[epoch]
-            loss_sum = np.zeros(k)
-            loss_cnt = np.zeros(k, dtype=np.int64)
-            for i, w in enumerate(tr.mine):  # python-float sums in iteration order
-                for it in range(tr.per_epoch):
-                    loss_sum[w] += losses[it, i]
-                    loss_cnt[w] += 1
-            if tr.world > 1:
-                ls = torch.as_tensor(loss_sum, device="cuda")
-                lc = torch.as_tensor(loss_cnt, device="cuda")
-                tr.dist.all_reduce(ls)
-                tr.dist.all_reduce(lc)
-                tr.dist.all_reduce(ledger)
-                loss_sum, loss_cnt = ls.cpu().numpy(), lc.cpu().numpy()
-            ledger_np = ledger.cpu().numpy()
-            logits = _predict_device(tr.dg, tr.wviews, tr.dims, tr.dtype)
-            preds = torch.argmax(logits, dim=1)
-            correct = (preds == labels_t).cpu().numpy()
-            val_acc = float(np.mean(correct[val_nodes])) if len(val_nodes) else 0.0
-            for w in range(k):
-                tw = tr.worker_train[w]
-                train_acc = float(np.mean(correct[tw])) if len(tw) else 0.0
-                mean_loss = float(loss_sum[w] / loss_cnt[w]) if loss_cnt[w] else 0.0
-                metrics.rows.append(MetricRow(epoch=epoch, worker=w, loss=mean_loss,
-                                              train_acc=train_acc, val_acc=val_acc,
-                                              comm_nodes_epoch=int(ledger_np[w].sum())))
+        pairs = [(e, it) for e in range(epochs) for it in range(tr.per_epoch)]
+        tr.run(pairs, on_iteration=end_of_epoch)
+        tr.check_errors()
         tr.weights_to_model()
         ledger_all = CommLedger(tr.ledger.cpu().numpy()[:epochs].copy())
     finally:
