@@ -156,10 +156,16 @@ int skg_adam_step(int dtype, uint64_t w_dev, uint64_t g_dev, uint64_t m_dev, uin
                   int64_t n, double lr, double contributors, int64_t t, void* stream);
 int skg_zero(int dtype, uint64_t p_dev, int64_t n, void* stream);
 
+/* fp32 GEMM engine: 0 = SIMT FP32, 1 = tcgen05 1xTF32, 3 = tcgen05 3xTF32 (default). */
+int skg_set_gemm_mode(int mode);
+
 /* ---------------------------------------------------------------- test hooks
  * Synchronous: numpy pairwise sum (total) and the exact sequential cumsum (cdf, T =
  * cdf[-1]) of a positive host array a[n], through the sampler's own kernels. */
 int skg_debug_reduce(const double* a, int64_t n, double* cdf, double* total, double* T);
+/* Synchronous: C = op(A) op(B) (row-major host arrays) with the given GEMM mode. */
+int skg_debug_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A, const float* B,
+                   float* C);
 
 #ifdef __cplusplus
 }

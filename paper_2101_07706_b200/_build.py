@@ -22,6 +22,7 @@ PER_FILE = {
     "sampler.cu": ["--fmad=false"],
     "capi.cu": ["--fmad=false"],
     "gcn.cu": [],
+    "gemm_tc.cu": [],
 }
 
 

@@ -79,6 +79,9 @@ _sig("skg_sgd_step", C.c_int, C.c_int, u64, u64, i64, dbl, dbl, vp)
 _sig("skg_adam_step", C.c_int, C.c_int, u64, u64, u64, u64, i64, dbl, dbl, i64, vp)
 _sig("skg_zero", C.c_int, C.c_int, u64, i64, vp)
 _sig("skg_debug_reduce", C.c_int, P(dbl), i64, P(dbl), P(dbl), P(dbl))
+_sig("skg_debug_gemm", C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, P(C.c_float),
+     P(C.c_float), P(C.c_float))
+_sig("skg_set_gemm_mode", C.c_int, C.c_int)
 
 # every symbol the public header declares (checked by tests/test_native_abi.py)
 EXPORTED = [
@@ -89,7 +92,7 @@ EXPORTED = [
     "skg_plans_create", "skg_plans_destroy", "skg_ladies_sample", "skg_ladies_sample_device", "skg_saint_set_candidates",
     "skg_saint_sample", "skg_plan_stats", "skg_plan_layer", "skg_gcn_create", "skg_gcn_destroy",
     "skg_gcn_step", "skg_gcn_step_batch", "skg_gcn_forward", "skg_gcn_read_logits", "skg_predict_logits",
-    "skg_sgd_step", "skg_adam_step", "skg_zero", "skg_debug_reduce",
+    "skg_sgd_step", "skg_adam_step", "skg_zero", "skg_debug_reduce", "skg_debug_gemm", "skg_set_gemm_mode",
 ]
 
 

@@ -1187,6 +1187,13 @@ extern "C" int skg_adam_step(int dtype, uint64_t w, uint64_t g, uint64_t m, uint
   return SKG_OK;
 }
 
+namespace skg { extern int g_gemm_mode; }
+extern "C" int skg_set_gemm_mode(int mode) {
+  ARG(mode == 0 || mode == 1 || mode == 3, "gemm mode must be 0 (SIMT), 1 (TF32) or 3 (3xTF32)");
+  skg::g_gemm_mode = mode;
+  return SKG_OK;
+}
+
 extern "C" int skg_zero(int dtype, uint64_t p, int64_t n, void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
   if (dtype == DT_F32) fill_zero<float>((float*)p, n, st);

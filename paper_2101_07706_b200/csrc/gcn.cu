@@ -257,11 +257,22 @@ static void gemm_launch(bool ta, bool tb, int n, int M, int N, int K, const int3
   else GLAUNCH((k_gemm_b<T, true, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
 }
 
+int g_gemm_mode = 3;  // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
+int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+            const int32_t* const* dK, Act<float> A, Act<float> B, Act<float> C, bool acc,
+            cudaStream_t st);
+
 template <typename T>
 void gemm_b(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
             const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool accumulate,
             cudaStream_t st) {
   if (M <= 0 || N <= 0 || n <= 0) return;
+  if constexpr (sizeof(T) == 4) {
+    if (g_gemm_mode != 0) {
+      gemm_tc(g_gemm_mode, ta, tb, n, M, N, K, dM, dK, A, B, C, accumulate, st);
+      return;
+    }
+  }
   if (sizeof(T) == 4 && N > 32)
     gemm_launch<T, 128, 64, 16, 8, 4>(ta, tb, n, M, N, K, dM, dK, A, B, C, accumulate, st);
   else
@@ -272,7 +283,14 @@ template <typename T>
 void gemm_plain(int M, int N, int K, const T* A, int64_t lda, const T* B, int64_t ldb, T* C,
                 int64_t ldc, cudaStream_t st) {
   Act<T> a{const_cast<T*>(A), 0, lda}, b{const_cast<T*>(B), 0, ldb}, c{C, 0, ldc};
-  gemm_b<T>(false, false, 1, M, N, K, nullptr, nullptr, a, b, c, false, st);
+  // full-graph inference: M = n rows, split into grid-y chunks the hardware accepts
+  const int chunk = 65535 * 64;
+  for (int m0 = 0; m0 < M; m0 += chunk) {
+    Act<T> a2 = a, c2 = c;
+    a2.base += (int64_t)m0 * lda;
+    c2.base += (int64_t)m0 * ldc;
+    gemm_b<T>(false, false, 1, std::min(chunk, M - m0), N, K, nullptr, nullptr, a2, b, c2, false, st);
+  }
 }
 
 // deterministic split-K reduction: C (+)= P_0 + P_1 + ... in slot order

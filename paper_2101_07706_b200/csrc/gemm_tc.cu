@@ -1,0 +1,305 @@
+// tcgen05 (5th-gen tensor core) GEMM for the GCN's dense contractions H·W, G·Wᵀ, Uᵀ·G.
+//
+// One CTA (4 warps) owns a 128 x BN output tile whose fp32 accumulator lives in TMEM.
+// Operands are read from global memory (any of the four transpositions), split into
+// TF32 hi/lo parts and staged in shared memory in the canonical no-swizzle K-major UMMA
+// layout (8-row x 16-byte core matrices; LBO = next core matrix along K, SBO = next along
+// M/N).  Thread 0 issues tcgen05.mma.kind::tf32 for each K step and commits to an
+// mbarrier per stage, so the loads of stage s+1 overlap the MMAs of stage s.
+//   MODE 1: 1xTF32 (10-bit mantissa inputs)
+//   MODE 3: 3xTF32  D += Ahi Bhi + Ahi Blo + Alo Bhi  (~fp32 accuracy; default, keeps the
+//           rtol 1e-4 parity of fp32 activations/gradients against the fp64 reference)
+#include <cstdint>
+#include <cstdio>
+
+#include "gcn.cuh"
+#include "sampler.cuh"
+#include "skg_internal.h"
+
+namespace skg {
+
+namespace tc {
+
+constexpr int BM = 128;
+constexpr int BK = 32;                 // K elements per stage (4 MMAs of K = 8)
+constexpr int KGROUPS = BK / 4;        // core matrices along K per stage
+constexpr int NTHREADS = 128;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// canonical K-major, no swizzle: element (row, k) of a tile with `rows` rows
+__device__ __forceinline__ int kmaj_off(int row, int k) {
+  return (((row >> 3) * KGROUPS + (k >> 2)) << 5) + ((row & 7) << 2) + (k & 3);
+}
+
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+  const uint64_t lbo = 128, sbo = (uint64_t)KGROUPS * 128;
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  return d;                // base offset 0, legacy LBO mode, SWIZZLE_NONE
+}
+
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
+  // c_format F32 (bit 4), a/b format TF32 (=2 at bits 7, 10), K-major A and B,
+  // n_dim = N >> 3 at bit 17, m_dim = M >> 4 at bit 24
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm volatile("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity));
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+      smem_u32(bar)));
+}
+
+template <bool TRANS, int ROWS>
+__device__ __forceinline__ void load_stage(const float* __restrict__ src, int64_t ld, int row0,
+                                           int nrows, int k0, int K, float* s_hi, float* s_lo,
+                                           bool split) {
+  // tile element (r, k) = TRANS ? src[(k0+k)*ld + row0 + r] : src[(row0+r)*ld + k0 + k]
+  constexpr int ELEMS = ROWS * BK;
+#pragma unroll 4
+  for (int idx = threadIdx.x; idx < ELEMS; idx += NTHREADS) {
+    int r, k;
+    if (TRANS) {
+      k = idx / ROWS;
+      r = idx % ROWS;
+    } else {
+      r = idx / BK;
+      k = idx % BK;
+    }
+    const int gr = row0 + r, gk = k0 + k;
+    float v = 0.f;
+    if (gr < nrows && gk < K) v = TRANS ? src[(int64_t)gk * ld + gr] : src[(int64_t)gr * ld + gk];
+    const float hi = to_tf32(v);
+    const int o = kmaj_off(r, k);
+    s_hi[o] = hi;
+    if (split) s_lo[o] = to_tf32(v - hi);
+  }
+}
+
+}  // namespace tc
+
+// C_z = op(A_z) op(B_z) (+ C_z) on tensor cores; op(A) M x K, op(B) K x N.
+template <bool TA, bool TB, int BN, int MODE>
+__global__ void __launch_bounds__(tc::NTHREADS, 1)
+    k_gemm_tc(int Mfix, int N, int Kfix, const int32_t* const* dM, const int32_t* const* dK,
+              Act<float> A, Act<float> B, Act<float> C, int accumulate) {
+  using namespace tc;
+  constexpr bool SPLIT = MODE == 3;
+  constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
+  constexpr int STAGE = (A_ELEMS + B_ELEMS) * (SPLIT ? 2 : 1);
+  constexpr int TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  extern __shared__ __align__(1024) float smem[];
+  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ uint32_t tmem_base;
+
+  const int z = blockIdx.z;
+  const int M = dM ? *dM[z] : Mfix;
+  const int K = dK ? *dK[z] : Kfix;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  if (m0 >= M) return;
+  const float* __restrict__ a = A.at(z);
+  const float* __restrict__ b = B.at(z);
+  float* __restrict__ c = C.at(z);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "n"(TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+  constexpr uint32_t idesc = make_idesc(BM, BN);
+
+  const int nk = (K + BK - 1) / BK;
+  uint32_t phase[2] = {0u, 0u};
+  for (int kc = 0; kc < nk; ++kc) {
+    const int s = kc & 1;
+    float* st = smem + s * STAGE;
+    float* a_hi = st;
+    float* b_hi = st + A_ELEMS;
+    float* a_lo = st + A_ELEMS + B_ELEMS;
+    float* b_lo = a_lo + A_ELEMS;
+    if (kc >= 2) {  // the MMAs that read this stage two chunks ago must be done
+      mbar_wait(&bars[s], phase[s]);
+      phase[s] ^= 1u;
+    }
+    load_stage<TA, BM>(a, A.ld, m0, M, kc * BK, K, a_hi, a_lo, SPLIT);
+    load_stage<!TB, BN>(b, B.ld, n0, N, kc * BK, K, b_hi, b_lo, SPLIT);
+    asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy smem writes -> tensor core
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;");
+#pragma unroll
+      for (int ks = 0; ks < BK / 8; ++ks) {
+        const uint32_t koff = ks * 2 * 128;  // two core matrices along K per MMA
+        const uint64_t ah = make_desc(smem_u32(a_hi) + koff);
+        const uint64_t bh = make_desc(smem_u32(b_hi) + koff);
+        const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
+        mma_tf32(tmem, ah, bh, idesc, acc);
+        if (SPLIT) {
+          const uint64_t al = make_desc(smem_u32(a_lo) + koff);
+          const uint64_t bl = make_desc(smem_u32(b_lo) + koff);
+          mma_tf32(tmem, ah, bl, idesc, 1u);
+          mma_tf32(tmem, al, bh, idesc, 1u);
+        }
+      }
+      mma_commit(&bars[s]);
+    }
+    __syncthreads();
+  }
+  // wait for the last commit of each used stage
+  if (nk >= 1) {
+    const int s = (nk - 1) & 1;
+    mbar_wait(&bars[s], phase[s]);
+  }
+  if (nk >= 2) {
+    const int s = nk & 1;  // the other stage's last commit (already complete or pending)
+    mbar_wait(&bars[s], phase[s]);
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  // epilogue: warp w reads TMEM lanes [32w, 32w+32) = tile rows
+  const int row = m0 + warp * 32 + lane;
+  const uint32_t taddr_row = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int cb = 0; cb < BN; cb += 16) {
+    uint32_t v[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr_row + cb));
+    asm volatile("tcgen05.wait::ld.sync.aligned;");
+    if (row < M) {
+      float* crow = c + (int64_t)row * C.ld;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int col = n0 + cb + j;
+        if (col < N) crow[col] = accumulate ? crow[col] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
+}
+
+template <bool TA, bool TB, int BN, int MODE>
+static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
+                     Act<float> A, Act<float> B, Act<float> C, bool acc, cudaStream_t st) {
+  constexpr int STAGE = (tc::BM * tc::BK + BN * tc::BK) * (MODE == 3 ? 2 : 1);
+  const size_t smem = (size_t)2 * STAGE * sizeof(float);
+  auto kern = k_gemm_tc<TA, TB, BN, MODE>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  dim3 grid((N + BN - 1) / BN, (M + tc::BM - 1) / tc::BM, n);
+  kern<<<grid, tc::NTHREADS, smem, st>>>(M, N, K, dM, dK, A, B, C, acc ? 1 : 0);
+  ++g_kernel_launches;
+  return 0;
+}
+
+template <bool TA, bool TB, int MODE>
+static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
+                       Act<float> A, Act<float> B, Act<float> C, bool acc, cudaStream_t st) {
+  if (N <= 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  if (N <= 64) return launch_tc<TA, TB, 64, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  if (N <= 128) return launch_tc<TA, TB, 128, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  return launch_tc<TA, TB, 256, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+}
+
+int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+            const int32_t* const* dK, Act<float> A, Act<float> B, Act<float> C, bool acc,
+            cudaStream_t st) {
+  if (M <= 0 || N <= 0 || n <= 0) return 0;
+#define TC_CASE(TA_, TB_)                                                                        \
+  if (ta == TA_ && tb == TB_)                                                                    \
+    return mode == 3 ? dispatch_bn<TA_, TB_, 3>(n, M, N, K, dM, dK, A, B, C, acc, st)            \
+                     : dispatch_bn<TA_, TB_, 1>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  TC_CASE(false, false)
+  TC_CASE(true, false)
+  TC_CASE(false, true)
+  TC_CASE(true, true)
+#undef TC_CASE
+  return 0;
+}
+
+// test hook: C = op(A) op(B) for host arrays (row-major, ld = inner dim)
+int debug_gemm(int mode, int ta, int tb, int M, int N, int K, const float* hA, const float* hB,
+               float* hC) {
+  const size_t na = (size_t)M * K, nb = (size_t)K * N, nc = (size_t)M * N;
+  float *dA, *dB, *dC;
+  cudaMalloc(&dA, na * 4);
+  cudaMalloc(&dB, nb * 4);
+  cudaMalloc(&dC, nc * 4);
+  cudaMemcpy(dA, hA, na * 4, cudaMemcpyHostToDevice);
+  cudaMemcpy(dB, hB, nb * 4, cudaMemcpyHostToDevice);
+  cudaMemset(dC, 0, nc * 4);
+  Act<float> a{dA, 0, ta ? M : K}, b{dB, 0, tb ? K : N}, c{dC, 0, N};
+  if (mode == 0) gemm_b<float>(ta, tb, 1, M, N, K, nullptr, nullptr, a, b, c, false, 0);
+  else gemm_tc(mode, ta, tb, 1, M, N, K, nullptr, nullptr, a, b, c, false, 0);
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaMemcpy(hC, dC, nc * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dC);
+  if (e != cudaSuccess) {
+    set_error(std::string("debug_gemm: ") + cudaGetErrorString(e));
+    return SKG_ERR_CUDA;
+  }
+  return SKG_OK;
+}
+
+}  // namespace skg
+
+extern "C" int skg_debug_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A,
+                              const float* B, float* C) {
+  return skg::debug_gemm(mode, ta, tb, M, N, K, A, B, C);
+}

@@ -1,0 +1,52 @@
+"""Kernel-level GPU checks: tcgen05 GEMM modes against an fp64 numpy reference."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(mode, ta, tb, A, B, M, N, K):
+    from paper_2101_07706_b200._native import check, lib, ptr
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    B = np.ascontiguousarray(B, dtype=np.float32)
+    Cm = np.zeros((M, N), dtype=np.float32)
+    check(lib.skg_debug_gemm(mode, int(ta), int(tb), M, N, K, ptr(A, C.c_float), ptr(B, C.c_float),
+                             ptr(Cm, C.c_float)))
+    return Cm
+
+
+SHAPES = [(512, 256, 602), (512, 41, 256), (602, 256, 512), (256, 41, 509), (130, 17, 33),
+          (1, 256, 8), (4096, 256, 256), (300, 300, 1)]
+
+
+@pytest.mark.parametrize("mode,tol", [(0, 1e-5), (1, 3e-3), (3, 1e-5)])
+@pytest.mark.parametrize("ta", [False, True])
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_modes(mode, tol, ta, tb, shape):
+    M, N, K = shape
+    r = np.random.default_rng(M * 7 + N * 3 + K)
+    a = r.normal(size=(M, K)).astype(np.float32)
+    b = r.normal(size=(K, N)).astype(np.float32)
+    A = a.T.copy() if ta else a
+    B = b.T.copy() if tb else b
+    got = _gemm(mode, ta, tb, A, B, M, N, K)
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    # error relative to the magnitude of the dot products (norm-aware, no cancellation bias)
+    scale = np.abs(a).astype(np.float64) @ np.abs(b).astype(np.float64) + 1e-30
+    err = np.abs(got - ref) / scale
+    assert err.max() < tol, (mode, err.max())
+
+
+def test_gemm_3xtf32_beats_1xtf32():
+    M, N, K = 512, 256, 602
+    r = np.random.default_rng(1)
+    a = r.normal(size=(M, K)).astype(np.float32)
+    b = r.normal(size=(K, N)).astype(np.float32)
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    e1 = np.abs(_gemm(1, False, False, a, b, M, N, K) - ref).max()
+    e3 = np.abs(_gemm(3, False, False, a, b, M, N, K) - ref).max()
+    assert e3 * 50 < e1
