@@ -89,37 +89,76 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       smem_u32(bar)));
 }
 
+// Stage loads are split in two halves so the global loads of chunk k+1 are in flight
+// while chunk k is converted, fenced and multiplied: gload issues every load of the
+// stage into registers (QUADS/NTHREADS float4 per thread, all independent), sstore
+// converts them to TF32 hi/lo and writes the canonical K-major layout.
 template <bool TRANS, int ROWS>
-__device__ __forceinline__ void load_stage(const float* __restrict__ src, int64_t ld, int row0,
-                                           int nrows, int k0, int K, float* s_hi, float* s_lo,
-                                           bool split) {
-  // tile element (r, k) = TRANS ? src[(k0+k)*ld + row0 + r] : src[(row0+r)*ld + k0 + k]
-  constexpr int ELEMS = ROWS * BK;
-#pragma unroll 4
-  for (int idx = threadIdx.x; idx < ELEMS; idx += NTHREADS) {
-    int r, k;
+struct StageIO {
+  static constexpr int Q = ROWS * BK / 4 / NTHREADS;  // float4 quads per thread
+  // Each quad is 4 consecutive k of one tile row, stored as one 16-byte smem write.
+  // Thread mapping keeps both sides efficient: the 8 lanes of a warp that share a k
+  // group cover the 8 rows of one core matrix (a full 128-byte smem row, conflict-free),
+  // and global reads stay coalesced (TRANS: lanes walk the contiguous row axis).
+  __device__ static void coords(int q, int& r, int& k) {
+    const int qd = threadIdx.x + q * NTHREADS;
     if (TRANS) {
-      k = idx / ROWS;
-      r = idx % ROWS;
+      r = qd % ROWS;
+      k = (qd / ROWS) * 4;
     } else {
-      r = idx / BK;
-      k = idx % BK;
+      r = (qd & 7) + 8 * (qd >> 6);
+      k = ((qd >> 3) & 7) * 4;
     }
-    const int gr = row0 + r, gk = k0 + k;
-    float v = 0.f;
-    if (gr < nrows && gk < K) v = TRANS ? src[(int64_t)gk * ld + gr] : src[(int64_t)gr * ld + gk];
-    const float hi = to_tf32(v);
-    const int o = kmaj_off(r, k);
-    s_hi[o] = hi;
-    if (split) s_lo[o] = to_tf32(v - hi);
   }
-}
+  // tile element (r, k) = TRANS ? src[(k0+k)*ld + row0 + r] : src[(row0+r)*ld + k0 + k]
+  __device__ static void gload(const float* __restrict__ src, int64_t ld, int row0, int nrows,
+                               int k0, int K, bool vec, float4 (&v)[Q]) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      int r, k;
+      coords(q, r, k);
+      const int gr = row0 + r, gk = k0 + k;
+      float t[4];
+      if (TRANS) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          t[e] = (gr < nrows && gk + e < K) ? __ldg(src + (int64_t)(gk + e) * ld + gr) : 0.f;
+      } else {
+        if (vec && gr < nrows && gk + 3 < K) {
+          v[q] = __ldg(reinterpret_cast<const float4*>(src + (int64_t)gr * ld + gk));
+          continue;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          t[e] = (gr < nrows && gk + e < K) ? __ldg(src + (int64_t)gr * ld + gk + e) : 0.f;
+      }
+      v[q] = make_float4(t[0], t[1], t[2], t[3]);
+    }
+  }
+  __device__ static void sstore(const float4 (&v)[Q], float* s_hi, float* s_lo, bool split) {
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      int r, k;
+      coords(q, r, k);
+      const float x[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
+      float hi[4], lo[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        hi[e] = to_tf32(x[e]);
+        lo[e] = to_tf32(x[e] - hi[e]);
+      }
+      const int o = kmaj_off(r, k);
+      *reinterpret_cast<float4*>(s_hi + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
+      if (split) *reinterpret_cast<float4*>(s_lo + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
+    }
+  }
+};
 
 }  // namespace tc
 
 // C_z = op(A_z) op(B_z) (+ C_z) on tensor cores; op(A) M x K, op(B) K x N.
 template <bool TA, bool TB, int BN, int MODE>
-__global__ void __launch_bounds__(tc::NTHREADS, 1)
+__global__ void __launch_bounds__(tc::NTHREADS)
     k_gemm_tc(int Mfix, int N, int Kfix, const int32_t* const* dM, const int32_t* const* dK,
               Act<float> A, Act<float> B, Act<float> C, int accumulate) {
   using namespace tc;
@@ -140,6 +179,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   const float* __restrict__ b = B.at(z);
   float* __restrict__ c = C.at(z);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool vecA = (A.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
+  const bool vecB = (B.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -160,6 +201,13 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
 
   const int nk = (K + BK - 1) / BK;
   uint32_t phase[2] = {0u, 0u};
+  using IOA = StageIO<TA, BM>;
+  using IOB = StageIO<!TB, BN>;
+  float4 ra[IOA::Q], rb[IOB::Q];
+  if (nk > 0) {
+    IOA::gload(a, A.ld, m0, M, 0, K, vecA, ra);
+    IOB::gload(b, B.ld, n0, N, 0, K, vecB, rb);
+  }
   for (int kc = 0; kc < nk; ++kc) {
     const int s = kc & 1;
     float* st = smem + s * STAGE;
@@ -171,8 +219,12 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
       mbar_wait(&bars[s], phase[s]);
       phase[s] ^= 1u;
     }
-    load_stage<TA, BM>(a, A.ld, m0, M, kc * BK, K, a_hi, a_lo, SPLIT);
-    load_stage<!TB, BN>(b, B.ld, n0, N, kc * BK, K, b_hi, b_lo, SPLIT);
+    IOA::sstore(ra, a_hi, a_lo, SPLIT);
+    IOB::sstore(rb, b_hi, b_lo, SPLIT);
+    if (kc + 1 < nk) {  // next chunk's loads fly during the barrier and the MMAs
+      IOA::gload(a, A.ld, m0, M, (kc + 1) * BK, K, vecA, ra);
+      IOB::gload(b, B.ld, n0, N, (kc + 1) * BK, K, vecB, rb);
+    }
     asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy smem writes -> tensor core
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -193,7 +245,6 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
       }
       mma_commit(&bars[s]);
     }
-    __syncthreads();
   }
   // wait for the last commit of each used stage
   if (nk >= 1) {
@@ -249,10 +300,9 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
 template <bool TA, bool TB, int MODE>
 static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
                        Act<float> A, Act<float> B, Act<float> C, bool acc, cudaStream_t st) {
+  // narrow N tiles: more CTAs for these skinny problems (M <= a few thousand rows)
   if (N <= 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
-  if (N <= 64) return launch_tc<TA, TB, 64, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
-  if (N <= 128) return launch_tc<TA, TB, 128, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
-  return launch_tc<TA, TB, 256, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  return launch_tc<TA, TB, 64, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
 }
 
 int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
