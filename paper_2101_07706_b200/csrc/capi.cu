@@ -52,6 +52,8 @@ struct skg_ctx {
   int32_t* d_trow = nullptr;
   double* d_tw = nullptr;
   bool symmetric = true;
+  bool normalized = false;
+  double* d_degd = nullptr;
   std::vector<int64_t> deg_desc_prefix;  // prefix sums of degrees sorted descending
   void* d_x = nullptr;
   int64_t F = 0, ldx = 0, x_rows = 0;
@@ -73,6 +75,8 @@ struct skg_ctx {
     g.t_row = symmetric ? d_col : d_trow;
     g.t_w = symmetric ? d_w : d_tw;
     g.n_words = (int32_t)((n + 31) / 32);
+    g.normalized = normalized ? 1 : 0;
+    g.degd = d_degd;
     return g;
   }
   FeatStore fstore() const {
@@ -151,6 +155,24 @@ __global__ void k_check_symmetric(int64_t n, const int64_t* off, const int32_t* 
       if (lo >= off[j + 1] || col[lo] != i ||
           __double_as_longlong(w[lo]) != __double_as_longlong(w[e]))
         atomicExch(bad, 1);
+    }
+  }
+}
+
+// normalised-graph check: w[e] == 1.0/sqrt(d_i * d_j) bit for bit (graph.py:180-182)
+__global__ void k_check_normalized(int64_t n, const int64_t* off, const int32_t* col,
+                                   const double* w, double* degd, int* bad) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    degd[i] = (double)(off[i + 1] - off[i]);
+  __syncthreads();
+}
+__global__ void k_check_normalized2(int64_t n, const int64_t* off, const int32_t* col,
+                                    const double* w, const double* degd, int* bad) {
+  for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
+    for (int64_t e = off[i] + threadIdx.x; e < off[i + 1]; e += blockDim.x) {
+      const double x = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(degd[i], degd[col[e]])));
+      if (__double_as_longlong(x) != __double_as_longlong(w[e])) atomicExch(bad, 1);
     }
   }
 }
@@ -266,8 +288,16 @@ extern "C" int skg_ctx_create(int device, int64_t n, int64_t nnz, const int64_t*
   if (n) k_check_symmetric<<<std::min<int64_t>(n, 65535), 256>>>(n, c->d_off, c->d_col, c->d_w, d_bad);
   int bad = 0;
   CK(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
-  cudaFree(d_bad);
   c->symmetric = !bad;
+  CK(cudaMalloc(&c->d_degd, sizeof(double) * std::max<int64_t>(n, 1)));
+  CK(cudaMemset(d_bad, 0, sizeof(int)));
+  if (n) {
+    k_check_normalized<<<std::min<int64_t>((n + 255) / 256, 4096), 256>>>(n, c->d_off, c->d_col, c->d_w, c->d_degd, d_bad);
+    k_check_normalized2<<<std::min<int64_t>(n, 65535), 256>>>(n, c->d_off, c->d_col, c->d_w, c->d_degd, d_bad);
+  }
+  CK(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
+  c->normalized = (n > 0) && !bad;
+  cudaFree(d_bad);
   if (!c->symmetric) {  // host counting sort by column (rows ascending within a column)
     std::vector<int64_t> toff(n + 1, 0);
     for (int64_t e = 0; e < nnz; ++e) toff[neighbors[e] + 1]++;
@@ -303,6 +333,7 @@ extern "C" int skg_ctx_destroy(skg_ctx* c) {
   cudaFree(c->d_toff);
   cudaFree(c->d_trow);
   cudaFree(c->d_tw);
+  cudaFree(c->d_degd);
   cudaFree(c->d_x);
   cudaFree(c->d_labels);
   cudaFree(c->d_shards);
@@ -397,7 +428,7 @@ extern "C" int skg_ctx_info(skg_ctx* c, int64_t out[8]) {
   out[4] = c->F;
   out[5] = c->dtype;
   out[6] = c->device;
-  out[7] = c->n_ranks;
+  out[7] = c->n_ranks | ((int64_t)c->normalized << 32);
   return SKG_OK;
 }
 
@@ -500,16 +531,16 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     P.cap_tiles = cap_tiles;
     cv.add(P.bitmap, n_words);
     cv.add(P.sbitmap, n_words);
-    cv.add(P.cnt_node, std::max<int64_t>(n, 1));
+    cv.add(P.cnt_pack, (size_t)(n / 2 + 1));
+    cv.add(P.fill, kind == KIND_LADIES ? cap_cand : 1);
     cv.add(P.pair_off, cap_rows + 1);
-    cv.add(P.pair_slot, kind == KIND_LADIES ? cap_pairs : 1);
     cv.add(P.word_prefix, n_words);
     cv.add(P.tile_a, cap_tiles);
     cv.add(P.tile_b, cap_tiles);
     cv.add(P.tile_c, cap_tiles);
     cv.add(P.bucket_off, kind == KIND_LADIES ? cap_cand + 1 : 1);
     cv.add(P.bucket_r, kind == KIND_LADIES ? cap_pairs : 1);
-    cv.add(P.bucket_w, kind == KIND_LADIES ? cap_pairs : 1);
+    cv.add(P.bucket_w, (kind == KIND_LADIES && !c->normalized) ? cap_pairs : 1);
     cv.add(P.big_list, kind == KIND_LADIES ? cap_cand : 1);
     cv.add(P.pw_val, cap_slots);
     cv.add(P.pw_lvl, cap_slots);
@@ -524,7 +555,6 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     cv.add(P.super_mode, cap_supers);
     cv.add(P.super_start, cap_supers);
     cv.add(P.cdf, cap_cand);
-    cv.add(P.qarr, cap_cand);
     cv.add(P.draw_idx, budget);
     cv.add(P.cand, kind == KIND_LADIES ? (size_t)Ls * cap_cand : 1);
     cv.add(P.norm, (size_t)Ls * cap_cand);

@@ -21,6 +21,8 @@ struct GraphDev {
   const int32_t* t_row;
   const double* t_w;
   int32_t n_words;       // ceil(n/32)
+  int32_t normalized;    // every w_ij == 1/sqrt(d_i d_j) (graph.py:182), checked at load
+  const double* degd;    // [n] row lengths as double (normalized graphs)
 };
 
 // Per-layer scalars of one plan.  Layers are indexed top-down while sampling
@@ -63,16 +65,16 @@ struct PlanDev {
   // ---- scratch
   uint32_t* bitmap;         // [n_words]
   uint32_t* sbitmap;        // [n_words] sampled set
-  int32_t* cnt_node;        // [n], zero at rest
+  uint32_t* cnt_pack;       // [n/2+1] 16-bit pair counters per node, zero at rest
+  int32_t* fill;            // [cap_cand] bucket fill counters
   int64_t* pair_off;        // [cap_rows+1]
-  int32_t* pair_slot;       // [cap_pairs]
   int32_t* word_prefix;     // [n_words]
   int64_t* tile_a;          // [cap_tiles]
   int64_t* tile_b;          // [cap_tiles]
   int64_t* tile_c;          // [cap_tiles]
   int32_t* bucket_off;      // [cap_cand+1]
   int32_t* bucket_r;        // [cap_pairs]
-  double* bucket_w;         // [cap_pairs]
+  double* bucket_w;         // [cap_pairs] (only for graphs that are not normalised)
   int32_t* big_list;        // [cap_cand]
   int32_t* counters;        // [8]: 0 big_count
   double* pw_val;           // [cap_slots]
@@ -88,7 +90,6 @@ struct PlanDev {
   int32_t* super_mode;      // [cap_supers]
   double* super_start;      // [cap_supers]
   double* cdf;              // [cap_cand]
-  double* qarr;             // [cap_cand] q of the layer being sampled
   int32_t* draw_idx;        // [budget]
   int64_t* draws_consumed;  // [1] uniforms consumed by this plan so far
   int32_t* err;             // [1] ErrBits

@@ -314,3 +314,32 @@ def test_kernel_launch_counter_moves():
                     pkg.SamplerConfig(budget=5, mode="skewed", skew_constant=4.0), 3,
                     np.random.default_rng(0))
     assert pkg.kernel_launches() > before
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_unnormalised_asymmetric_graph_vs_oracle(seed):
+    """Arbitrary positive weights (not 1/sqrt(d_i d_j), not symmetric): the stored-weight
+    bucket path and the transposed (CSC) pull-norm path."""
+    pkg = P()
+    r = np.random.default_rng(700 + seed)
+    n = 800
+    m = 6000
+    u, v = r.integers(0, n, m), r.integers(0, n, m)
+    og = O.normalize_weights(O.graph_from_edge_array(np.stack([u, v], 1), n))
+    og.weights = r.uniform(0.05, 2.0, size=len(og.weights))   # break normalisation and symmetry
+    g = to_pkg_graph(og)
+    k = 3
+    opart = O.partition_nodes(n, k, "random", seed=seed)
+    part = pkg.Partition(n_workers=k, owner=opart.owner)
+    for mode, D in (("full", 0.0), ("skewed", 8.0), ("local", 0.0)):
+        ocfg = O.SamplerConfig(budget=64, skew_constant=D, mode=mode)
+        cfg = pkg.SamplerConfig(budget=64, skew_constant=D, mode=mode)
+        batch = opart.owned_by(1)[:50]
+        exp = O.ladies_plan(og, opart, 1, batch, ocfg, 3, np.random.default_rng(seed))
+        got = pkg.ladies_plan(g, part, 1, batch, cfg, 3, np.random.default_rng(seed))
+        assert_plan_equal(plan_to_dict(got), plan_to_dict(exp), value_rtol=VAL_RTOL)
+        train = np.sort(r.choice(n, 300, replace=False))
+        norms = O.column_norms(og, train, train) if mode != "local" else None
+        exp_s = O.saint_plan(og, opart, 1, train, 40, ocfg, 2, np.random.default_rng(seed), norms=norms)
+        got_s = pkg.saint_plan(g, part, 1, train, 40, cfg, 2, np.random.default_rng(seed))
+        assert_plan_equal(plan_to_dict(got_s), plan_to_dict(exp_s), value_rtol=VAL_RTOL)
