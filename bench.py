@@ -72,7 +72,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -255,6 +255,11 @@ def run_ours(args):
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     achieved = alg_bytes / (samp * 1e-3) / 1e9
 
+    # ---- per-kernel live timing (CUDA events around every launch of one kernel, on its
+    # stream, over K timed steps) and algorithmic bytes / flops per launch
+    kern = kernel_table(lib, steps_resident, W, K, stats, tr, n_my, T, peaks)
+    top = max(kern, key=lambda r: r["total_ms"])
+
     # ---- e2e through the public API: host-derived inputs, H2D each step, loss D2H
     barrier()
     h2d = [0]
@@ -303,11 +308,16 @@ def run_ours(args):
             "gpu_launches": int(launches),
             "stages_ms_per_iter": {"sample": round(samp / T, 4),
                                    "gcn_fwd_bwd_step": round(float(np.median(comp_ms)), 4)},
-            "roofline": {"bound": "hbm", "kernel": f"sampler (LADIES, 5 layers x {T * n_my} plans, "
-                                                     "one batched launch sequence)",
-                         "achieved": round(achieved, 2), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 5), "traffic": None,
-                         "algorithmic_bytes": int(alg_bytes), "duration_ms": round(samp, 4)},
+            "roofline": {"bound": top["bound"], "kernel": top["kernel"],
+                         "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],
+                         "frac": top["frac"], "traffic": None,
+                         "per_launch": top["per_launch"], "avg_launch_us": top["avg_us"],
+                         "share_of_step": round(top["total_ms"] / ms, 4),
+                         "peak_source": "MEASURED_PEAKS.json"},
+            "kernels": kern,
+            "sampler_stage": {"achieved_gbs": round(achieved, 2), "frac": round(achieved / hbm, 5),
+                              "algorithmic_bytes": int(alg_bytes), "duration_ms": round(samp, 4),
+                              "plans": T * n_my},
             "e2e": {"value": round(1000.0 * K / e2e_ms, 3), "unit": "iters/s",
                     "h2d_bytes_per_step": int(h2d[0] // K), "d2h_bytes_per_step": 8 * n_my},
             "clocks": clk.summary(),
@@ -319,6 +329,59 @@ def run_ours(args):
     tr.close()
     if dist is not None:
         dist.destroy_process_group()
+    return out
+
+
+def kernel_table(lib, steps_resident, W, K, stats, tr, n_my, T, peaks):
+    """Event-time the main kernels over the K timed steps and relate each to its
+    algorithmic bytes (HBM-bound sampler kernels) or flops (tensor-core GEMM)."""
+    import torch
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tflops = float(peaks.get("bf16_tflops", 1590.0))
+    L = N_LAYERS
+    # per-plan-layer statistics of the last sampled group (T * n_my plans)
+    R = sum(int(st[t, 0]) for st in stats for t in range(L))
+    Nc = sum(int(st[t, 1]) for st in stats for t in range(L))
+    E = sum(int(st[t, 9]) for st in stats for t in range(L))
+    launches_per_group = L  # one launch per layer for each sampler kernel
+    models = {  # bytes per sampler launch (averaged over the layers of one group)
+        "k_lad_expand": (4 * E + 16 * R) / launches_per_group,
+        "k_lad_scatter": (8 * E + 16 * R) / launches_per_group,
+        "k_lad_fold": (4 * E + 24 * Nc) / launches_per_group,
+        "k_cs_maps": (9 * Nc + Nc // 2) / launches_per_group,
+        "k_bitmap_compact": (11 * Nc) / launches_per_group,
+    }
+    # GEMM flops per launch: 3 contractions per layer (no input-gradient GEMM at layer 0)
+    dims = tr.dims
+    rows = [sum(int(st[L - 1 - l, 0]) for st in stats) / T for l in range(L)]  # per iteration
+    gflop = sum(2 * rows[l] * dims[l] * dims[l + 1] * (3 if l > 0 else 2) for l in range(L))
+    n_gemm = 3 * L - 1
+    out = []
+    for name in list(models) + ["k_gemm_tc"]:
+        torch.cuda.synchronize()
+        lib.skg_profile_start(name.encode())
+        steps_resident(W, K)
+        tot = C.c_double()
+        cnt = C.c_int64()
+        lib.skg_profile_stop(C.byref(tot), C.byref(cnt))
+        if cnt.value == 0:
+            continue
+        avg_s = tot.value / cnt.value * 1e-3
+        if name == "k_gemm_tc":
+            per = gflop / n_gemm
+            ach = per / avg_s / 1e12
+            row = {"kernel": name + " (3xTF32 tcgen05; algorithmic flops, bf16 peak)",
+                   "bound": "tensor", "unit": "TFLOP/s", "peak": tflops,
+                   "per_launch": {"flops": int(per)}}
+        else:
+            per = models[name]
+            ach = per / avg_s / 1e9
+            row = {"kernel": f"{name} ({T * n_my} plans per launch)", "bound": "hbm",
+                   "unit": "GB/s", "peak": hbm, "per_launch": {"bytes": int(per)}}
+        row.update({"achieved": round(ach, 2), "frac": round(ach / row["peak"], 5),
+                    "avg_us": round(avg_s * 1e6, 2), "launches": int(cnt.value),
+                    "total_ms": round(tot.value, 4)})
+        out.append(row)
     return out
 
 

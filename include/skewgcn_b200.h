@@ -44,6 +44,10 @@ int skg_abi_version(void);
 const char* skg_last_error(void);
 unsigned long long skg_kernel_launches(void);
 int skg_device_count(void);
+/* Per-kernel timing: bracket every launch of `kernel_name` with CUDA events on its
+ * stream until skg_profile_stop, which synchronises and returns the summed time. */
+int skg_profile_start(const char* kernel_name);
+int skg_profile_stop(double* total_ms, int64_t* launches);
 
 /* ---------------------------------------------------------------- host RNG runtime
  * spawn_rng (seeding.py:17-27): SHA-256 of each label's repr -> SeedSequence -> PCG64.
@@ -77,6 +81,10 @@ int skg_ctx_set_features(skg_ctx* ctx, int dtype, int64_t dim, int64_t n_rows,
 int skg_ctx_set_feature_map(skg_ctx* ctx, int n_ranks, const uint64_t* shard_ptrs,
                             const int32_t* node_rank, const int32_t* node_row);
 int skg_ctx_feature_ptr(skg_ctx* ctx, uint64_t* out_ptr, int64_t* out_ld);
+/* Upload a feature shard (n_rows x dim host rows, the ctx's dtype) into its own device
+ * allocation (exportable with skg_ipc_handle); owned and freed by the ctx. */
+int skg_ctx_shard_upload(skg_ctx* ctx, const void* host_rows, int64_t n_rows,
+                         uint64_t* out_dev_ptr);
 int skg_ctx_set_labels(skg_ctx* ctx, const int64_t* labels);
 /* Replace the ownership map (Partition.owner) without re-uploading the CSR. */
 int skg_ctx_set_owner(skg_ctx* ctx, int32_t n_workers, const int32_t* owner);

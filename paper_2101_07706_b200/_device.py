@@ -145,6 +145,32 @@ class DeviceGraph:
                     lib.skg_gcn_destroy(g)
                 ps._gcn.clear()
 
+    def set_feature_shards(self, shard_ptrs, node_rank: np.ndarray, node_row: np.ndarray) -> None:
+        """Route layer-0 gathers through a table of shard base pointers (this rank's shard
+        or NVLink-mapped peer shards): node -> (rank, row).  Shards use the same padded row
+        stride and dtype as the features set with ensure_features."""
+        p = np.ascontiguousarray(np.asarray(shard_ptrs, dtype=np.uint64))
+        r = np.ascontiguousarray(node_rank, dtype=np.int32)
+        w = np.ascontiguousarray(node_row, dtype=np.int32)
+        if len(r) != self.n or len(w) != self.n:
+            raise ValueError("node_rank/node_row must cover every node")
+        check(lib.skg_ctx_set_feature_map(self.ctx, len(p), ptr(p, C.c_uint64), ptr(r, C.c_int32),
+                                          ptr(w, C.c_int32)))
+
+    def upload_shard(self, rows: np.ndarray, dtype: str) -> int:
+        """Copy host feature rows into their own device allocation (IPC-exportable)."""
+        host = np.ascontiguousarray(rows, dtype=np.float32 if dtype == "float32" else np.float64)
+        out = C.c_uint64()
+        check(lib.skg_ctx_shard_upload(self.ctx, host.ctypes.data_as(C.c_void_p), host.shape[0],
+                                       C.byref(out)))
+        return int(out.value)
+
+    def feature_ld(self) -> int:
+        out = C.c_uint64()
+        ld = C.c_int64()
+        check(lib.skg_ctx_feature_ptr(self.ctx, C.byref(out), C.byref(ld)))
+        return int(ld.value)
+
     def ensure_labels(self, labels: np.ndarray) -> None:
         key = (id(labels), labels.__array_interface__["data"][0], labels.shape)
         if key == self.lab_key:

@@ -10,10 +10,22 @@
 
 #include "../../include/skewgcn_b200.h"
 #include "gcn.cuh"
+#include "prof.h"
 #include "sampler.cuh"
 #include "skg_internal.h"
 
 namespace skg {
+static std::string g_prof_target;
+static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_pairs;
+static cudaEvent_t g_prof_open = nullptr;
+bool prof_match(const char* name) { return !g_prof_target.empty() && g_prof_target == name; }
+void prof_record(cudaStream_t st, bool before) {
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, st);
+  if (before) g_prof_open = e;
+  else g_prof_pairs.push_back({g_prof_open, e});
+}
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 const char* last_error() { return g_err.c_str(); }
@@ -63,6 +75,7 @@ struct skg_ctx {
   uint64_t* d_shards = nullptr;
   int32_t* d_node_rank = nullptr;
   int32_t* d_node_row = nullptr;
+  std::vector<void*> shards_owned;
   GraphDev gdev() const {
     GraphDev g;
     g.n = n;
@@ -184,6 +197,29 @@ __global__ void k_ids64_to_32(const int64_t* in, int64_t n, int32_t* out) {
 
 // ------------------------------------------------------------------ misc
 extern "C" int skg_abi_version(void) { return 1; }
+
+extern "C" int skg_profile_start(const char* kernel_name) {
+  g_prof_target = kernel_name ? kernel_name : "";
+  g_prof_pairs.clear();
+  return SKG_OK;
+}
+
+extern "C" int skg_profile_stop(double* total_ms, int64_t* launches) {
+  CK(cudaDeviceSynchronize());
+  double tot = 0.0;
+  for (auto& pr : g_prof_pairs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    tot += ms;
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+  *total_ms = tot;
+  *launches = (int64_t)g_prof_pairs.size();
+  g_prof_pairs.clear();
+  g_prof_target.clear();
+  return SKG_OK;
+}
 extern "C" const char* skg_last_error(void) { return last_error(); }
 extern "C" unsigned long long skg_kernel_launches(void) { return g_kernel_launches; }
 extern "C" int skg_device_count(void) {
@@ -339,6 +375,7 @@ extern "C" int skg_ctx_destroy(skg_ctx* c) {
   cudaFree(c->d_shards);
   cudaFree(c->d_node_rank);
   cudaFree(c->d_node_row);
+  for (void* p : c->shards_owned) cudaFree(p);
   delete c;
   return SKG_OK;
 }
@@ -385,6 +422,21 @@ extern "C" int skg_ctx_set_feature_map(skg_ctx* c, int n_ranks, const uint64_t* 
   CK(cudaMemcpy(c->d_node_rank, node_rank, sizeof(int32_t) * c->n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(c->d_node_row, node_row, sizeof(int32_t) * c->n, cudaMemcpyHostToDevice));
   c->n_ranks = n_ranks;
+  return SKG_OK;
+}
+
+extern "C" int skg_ctx_shard_upload(skg_ctx* c, const void* host_rows, int64_t n_rows,
+                                    uint64_t* out_dev_ptr) {
+  ARG(c && c->d_x && n_rows >= 0 && out_dev_ptr, "set features before uploading shards");
+  CK(cudaSetDevice(c->device));
+  const size_t es = c->dtype == DT_F32 ? 4 : 8;
+  void* p = nullptr;
+  CK(cudaMalloc(&p, es * c->ldx * std::max<int64_t>(n_rows, 1)));
+  CK(cudaMemset(p, 0, es * c->ldx * std::max<int64_t>(n_rows, 1)));
+  if (n_rows)
+    CK(cudaMemcpy2D(p, es * c->ldx, host_rows, es * c->F, es * c->F, n_rows, cudaMemcpyHostToDevice));
+  c->shards_owned.push_back(p);
+  *out_dev_ptr = (uint64_t)p;
   return SKG_OK;
 }
 
@@ -842,8 +894,8 @@ __global__ void k_ledger_add(const PlanDev* plans, int L, int64_t* ledger) {
 extern "C" int skg_plans_ledger_add(skg_plans* ps, int slot0, int n, uint64_t ledger_dev,
                                     void* stream) {
   ARG(ps && slot0 >= 0 && n >= 1 && slot0 + n <= ps->n_slots && ledger_dev, "bad ledger arguments");
-  k_ledger_add<<<n, 32, 0, (cudaStream_t)stream>>>(ps->d_plans + slot0, ps->L, (int64_t*)ledger_dev);
-  ++g_kernel_launches;
+  cudaStream_t st = (cudaStream_t)stream;
+  LAUNCH_NAMED("k_ledger_add", st, k_ledger_add<<<n, 32, 0, st>>>(ps->d_plans + slot0, ps->L, (int64_t*)ledger_dev));
   CK(cudaGetLastError());
   return SKG_OK;
 }

@@ -11,16 +11,13 @@
 #include <cstdio>
 
 #include "gcn.cuh"
+#include "prof.h"
 #include "sampler.cuh"
 #include "skg_internal.h"
 
 namespace skg {
 
-#define GLAUNCH(...)       \
-  do {                     \
-    __VA_ARGS__;           \
-    ++g_kernel_launches;   \
-  } while (0)
+
 
 constexpr unsigned FULLM = 0xffffffffu;
 
@@ -99,7 +96,7 @@ __global__ void k_gather_b(FeatStore fs, const SlotDesc* sd, Act<T> out) {
 template <typename T>
 void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows, Act<T> out,
                    cudaStream_t st) {
-  GLAUNCH(k_gather_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(fs, sd, out));
+  LAUNCH_NAMED("k_gather_b", st, k_gather_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(fs, sd, out));
 }
 
 // ------------------------------------------------------------------ SpMM (K8 / K10)
@@ -134,9 +131,9 @@ template <typename T>
 void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
             Act<T> H, Act<T> out, int64_t width, cudaStream_t st) {
   dim3 grid(row_blocks(max_rows, n), n);
-  if (transposed) GLAUNCH((k_spmm_b<T, true, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
-  else if (relu_in) GLAUNCH((k_spmm_b<T, false, true><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
-  else GLAUNCH((k_spmm_b<T, false, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
+  if (transposed) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, true, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
+  else if (relu_in) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, true><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
+  else LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
 }
 
 // full-graph SpMM for predict_logits (int64 offsets)
@@ -165,9 +162,9 @@ void spmm_full(int64_t n, const int64_t* off, const int32_t* col, const double* 
                int64_t lda, bool relu_in, T* out, int64_t ldo, int64_t width, cudaStream_t st) {
   int blocks = 16 * sms();
   if (relu_in)
-    GLAUNCH((k_spmm_full<T, true><<<blocks, 256, 0, st>>>(n, off, col, w, A, lda, out, ldo, width)));
+    LAUNCH_NAMED("k_spmm_full", st, (k_spmm_full<T, true><<<blocks, 256, 0, st>>>(n, off, col, w, A, lda, out, ldo, width)));
   else
-    GLAUNCH((k_spmm_full<T, false><<<blocks, 256, 0, st>>>(n, off, col, w, A, lda, out, ldo, width)));
+    LAUNCH_NAMED("k_spmm_full", st, (k_spmm_full<T, false><<<blocks, 256, 0, st>>>(n, off, col, w, A, lda, out, ldo, width)));
 }
 
 // ------------------------------------------------------------------ GEMM (K9)
@@ -251,10 +248,10 @@ static void gemm_launch(bool ta, bool tb, int n, int M, int N, int K, const int3
                         cudaStream_t st) {
   constexpr int NT = (BM / TM) * (BN / TN);
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, n);
-  if (!ta && !tb) GLAUNCH((k_gemm_b<T, false, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
-  else if (ta && !tb) GLAUNCH((k_gemm_b<T, true, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
-  else if (!ta && tb) GLAUNCH((k_gemm_b<T, false, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
-  else GLAUNCH((k_gemm_b<T, true, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  if (!ta && !tb) LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, false, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  else if (ta && !tb) LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, true, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  else if (!ta && tb) LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, false, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  else LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, true, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
 }
 
 int g_gemm_mode = 3;  // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
@@ -312,7 +309,7 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
                   int64_t ldp, T* C, int64_t ldc, bool accumulate, cudaStream_t st) {
   int64_t total = rows * cols;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * sms());
-  GLAUNCH((k_reduce_slots<T><<<std::max(blocks, 1), 256, 0, st>>>(parts, part_stride, n, rows, cols,
+  LAUNCH_NAMED("k_reduce_slots", st, (k_reduce_slots<T><<<std::max(blocks, 1), 256, 0, st>>>(parts, part_stride, n, rows, cols,
                                                                  ldp, C, ldc, accumulate)));
 }
 
@@ -392,9 +389,9 @@ __global__ void k_loss_mean(const SlotDesc* sd, const int32_t* labels, const dou
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
                   Act<T> G, double* row_loss, double* loss_out, cudaStream_t st) {
-  GLAUNCH((k_softmax_ce_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(
+  LAUNCH_NAMED("k_softmax_ce_b", st, (k_softmax_ce_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(
       sd, labels, Z, C, G, row_loss, max_rows)));
-  GLAUNCH((k_loss_mean<<<n, 256, 0, st>>>(sd, labels, row_loss, max_rows, loss_out)));
+  LAUNCH_NAMED("k_loss_mean", st, (k_loss_mean<<<n, 256, 0, st>>>(sd, labels, row_loss, max_rows, loss_out)));
 }
 
 // ------------------------------------------------------------------ optimizers (K12 epilogue)
@@ -436,7 +433,7 @@ __global__ void k_adam(T* w, const T* g, T* m, T* v, int64_t n, T lr, T contrib,
 template <typename T>
 void sgd_step(T* w, const T* g, int64_t n, double lr, double contrib, cudaStream_t st) {
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * sms());
-  GLAUNCH(k_sgd<T><<<std::max(blocks, 1), 256, 0, st>>>(w, g, n, (T)lr, (T)contrib));
+  LAUNCH_NAMED("k_sgd", st, k_sgd<T><<<std::max(blocks, 1), 256, 0, st>>>(w, g, n, (T)lr, (T)contrib));
 }
 
 template <typename T>
@@ -444,7 +441,7 @@ void adam_step(T* w, const T* g, T* m, T* v, int64_t n, double lr, double contri
                double b2, double omb1, double omb2, double bc1, double bc2, double eps,
                cudaStream_t st) {
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * sms());
-  GLAUNCH(k_adam<T><<<std::max(blocks, 1), 256, 0, st>>>(w, g, m, v, n, (T)lr, (T)contrib, (T)b1, (T)b2,
+  LAUNCH_NAMED("k_adam", st, k_adam<T><<<std::max(blocks, 1), 256, 0, st>>>(w, g, m, v, n, (T)lr, (T)contrib, (T)b1, (T)b2,
                                                          (T)omb1, (T)omb2, (T)bc1, (T)bc2, (T)eps));
 }
 
@@ -456,7 +453,7 @@ template <typename T>
 void fill_zero(T* p, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * sms());
-  GLAUNCH(k_zero<T><<<std::max(blocks, 1), 256, 0, st>>>(p, n));
+  LAUNCH_NAMED("k_zero", st, k_zero<T><<<std::max(blocks, 1), 256, 0, st>>>(p, n));
 }
 
 #define INST(T)                                                                                     \

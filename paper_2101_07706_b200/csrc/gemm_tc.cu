@@ -1,11 +1,15 @@
 // tcgen05 (5th-gen tensor core) GEMM for the GCN's dense contractions H·W, G·Wᵀ, Uᵀ·G.
 //
-// One CTA (4 warps) owns a 128 x BN output tile whose fp32 accumulator lives in TMEM.
-// Operands are read from global memory (any of the four transpositions), split into
-// TF32 hi/lo parts and staged in shared memory in the canonical no-swizzle K-major UMMA
-// layout (8-row x 16-byte core matrices; LBO = next core matrix along K, SBO = next along
-// M/N).  Thread 0 issues tcgen05.mma.kind::tf32 for each K step and commits to an
-// mbarrier per stage, so the loads of stage s+1 overlap the MMAs of stage s.
+// Warp-specialised, one 128 x BN output tile per CTA, fp32 accumulator in TMEM:
+//   warp 0      : TMEM allocation; lane 0 issues tcgen05.mma.kind::tf32 for every K step of
+//                 a full stage and commits it to that stage's "empty" mbarrier
+//   warps 1..8  : producers.  They read operands from global memory (any transposition),
+//                 split them into TF32 hi/lo parts and write the canonical no-swizzle
+//                 K-major UMMA layout (8-row x 16-byte core matrices; LBO = next core matrix
+//                 along K, SBO = next along M/N) into a STAGES-deep shared-memory ring, then
+//                 arrive on the stage's "full" mbarrier.  The next chunk's global loads are
+//                 issued before the current chunk is converted (register double buffer).
+//                 After the last commit they drain TMEM (tcgen05.ld) into global memory.
 //   MODE 1: 1xTF32 (10-bit mantissa inputs)
 //   MODE 3: 3xTF32  D += Ahi Bhi + Ahi Blo + Alo Bhi  (~fp32 accuracy; default, keeps the
 //           rtol 1e-4 parity of fp32 activations/gradients against the fp64 reference)
@@ -13,6 +17,7 @@
 #include <cstdio>
 
 #include "gcn.cuh"
+#include "prof.h"
 #include "sampler.cuh"
 #include "skg_internal.h"
 
@@ -23,13 +28,15 @@ namespace tc {
 constexpr int BM = 128;
 constexpr int BK = 32;                 // K elements per stage (4 MMAs of K = 8)
 constexpr int KGROUPS = BK / 4;        // core matrices along K per stage
-constexpr int NTHREADS = 128;
+constexpr int NPROD = 256;             // producer threads (8 warps)
+constexpr int NTHREADS = 32 + NPROD;
+constexpr int STAGES = 4;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// canonical K-major, no swizzle: element (row, k) of a tile with `rows` rows
+// canonical K-major, no swizzle: element (row, k) of a tile
 __device__ __forceinline__ int kmaj_off(int row, int k) {
   return (((row >> 3) * KGROUPS + (k >> 2)) << 5) + ((row & 7) << 2) + (k & 3);
 }
@@ -73,6 +80,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity));
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -89,19 +100,15 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       smem_u32(bar)));
 }
 
-// Stage loads are split in two halves so the global loads of chunk k+1 are in flight
-// while chunk k is converted, fenced and multiplied: gload issues every load of the
-// stage into registers (QUADS/NTHREADS float4 per thread, all independent), sstore
-// converts them to TF32 hi/lo and writes the canonical K-major layout.
+// Each quad is 4 consecutive k of one tile row, stored as one 16-byte smem write.  The 8
+// lanes of a warp sharing a k group cover the 8 rows of one core matrix (a full 128-byte
+// smem row: conflict-free) and global reads stay coalesced (TRANS: lanes walk the
+// contiguous row axis).
 template <bool TRANS, int ROWS>
 struct StageIO {
-  static constexpr int Q = ROWS * BK / 4 / NTHREADS;  // float4 quads per thread
-  // Each quad is 4 consecutive k of one tile row, stored as one 16-byte smem write.
-  // Thread mapping keeps both sides efficient: the 8 lanes of a warp that share a k
-  // group cover the 8 rows of one core matrix (a full 128-byte smem row, conflict-free),
-  // and global reads stay coalesced (TRANS: lanes walk the contiguous row axis).
-  __device__ static void coords(int q, int& r, int& k) {
-    const int qd = threadIdx.x + q * NTHREADS;
+  static constexpr int Q = ROWS * BK / 4 / NPROD;  // float4 quads per producer thread
+  __device__ static void coords(int p, int q, int& r, int& k) {
+    const int qd = p + q * NPROD;
     if (TRANS) {
       r = qd % ROWS;
       k = (qd / ROWS) * 4;
@@ -111,12 +118,12 @@ struct StageIO {
     }
   }
   // tile element (r, k) = TRANS ? src[(k0+k)*ld + row0 + r] : src[(row0+r)*ld + k0 + k]
-  __device__ static void gload(const float* __restrict__ src, int64_t ld, int row0, int nrows,
-                               int k0, int K, bool vec, float4 (&v)[Q]) {
+  __device__ static void gload(int p, const float* __restrict__ src, int64_t ld, int row0,
+                               int nrows, int k0, int K, bool vec, float4 (&v)[Q]) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       int r, k;
-      coords(q, r, k);
+      coords(p, q, r, k);
       const int gr = row0 + r, gk = k0 + k;
       float t[4];
       if (TRANS) {
@@ -135,11 +142,11 @@ struct StageIO {
       v[q] = make_float4(t[0], t[1], t[2], t[3]);
     }
   }
-  __device__ static void sstore(const float4 (&v)[Q], float* s_hi, float* s_lo, bool split) {
+  __device__ static void sstore(int p, const float4 (&v)[Q], float* s_hi, float* s_lo, bool split) {
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
       int r, k;
-      coords(q, r, k);
+      coords(p, q, r, k);
       const float x[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
       float hi[4], lo[4];
 #pragma unroll
@@ -158,7 +165,7 @@ struct StageIO {
 
 // C_z = op(A_z) op(B_z) (+ C_z) on tensor cores; op(A) M x K, op(B) K x N.
 template <bool TA, bool TB, int BN, int MODE>
-__global__ void __launch_bounds__(tc::NTHREADS)
+__global__ void __launch_bounds__(tc::NTHREADS, 1)
     k_gemm_tc(int Mfix, int N, int Kfix, const int32_t* const* dM, const int32_t* const* dK,
               Act<float> A, Act<float> B, Act<float> C, int accumulate) {
   using namespace tc;
@@ -167,7 +174,7 @@ __global__ void __launch_bounds__(tc::NTHREADS)
   constexpr int STAGE = (A_ELEMS + B_ELEMS) * (SPLIT ? 2 : 1);
   constexpr int TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
   extern __shared__ __align__(1024) float smem[];
-  __shared__ __align__(8) uint64_t bars[2];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], done_bar;
   __shared__ uint32_t tmem_base;
 
   const int z = blockIdx.z;
@@ -179,102 +186,105 @@ __global__ void __launch_bounds__(tc::NTHREADS)
   const float* __restrict__ b = B.at(z);
   float* __restrict__ c = C.at(z);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const bool vecA = (A.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
-  const bool vecB = (B.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+  const int nk = (K + BK - 1) / BK;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base)),
                  "n"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (threadIdx.x == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;");
+    if (lane == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&full_bar[s], NPROD / 32);  // one arrive per producer warp
+        mbar_init(&empty_bar[s], 1);          // tcgen05.commit
+      }
+      mbar_init(&done_bar, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
-  constexpr uint32_t idesc = make_idesc(BM, BN);
 
-  const int nk = (K + BK - 1) / BK;
-  uint32_t phase[2] = {0u, 0u};
-  using IOA = StageIO<TA, BM>;
-  using IOB = StageIO<!TB, BN>;
-  float4 ra[IOA::Q], rb[IOB::Q];
-  if (nk > 0) {
-    IOA::gload(a, A.ld, m0, M, 0, K, vecA, ra);
-    IOB::gload(b, B.ld, n0, N, 0, K, vecB, rb);
-  }
-  for (int kc = 0; kc < nk; ++kc) {
-    const int s = kc & 1;
-    float* st = smem + s * STAGE;
-    float* a_hi = st;
-    float* b_hi = st + A_ELEMS;
-    float* a_lo = st + A_ELEMS + B_ELEMS;
-    float* b_lo = a_lo + A_ELEMS;
-    if (kc >= 2) {  // the MMAs that read this stage two chunks ago must be done
-      mbar_wait(&bars[s], phase[s]);
-      phase[s] ^= 1u;
-    }
-    IOA::sstore(ra, a_hi, a_lo, SPLIT);
-    IOB::sstore(rb, b_hi, b_lo, SPLIT);
-    if (kc + 1 < nk) {  // next chunk's loads fly during the barrier and the MMAs
-      IOA::gload(a, A.ld, m0, M, (kc + 1) * BK, K, vecA, ra);
-      IOB::gload(b, B.ld, n0, N, (kc + 1) * BK, K, vecB, rb);
-    }
-    asm volatile("fence.proxy.async.shared::cta;");  // generic-proxy smem writes -> tensor core
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;");
+  if (warp == 0) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BM, BN);
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % STAGES;
+        mbar_wait(&full_bar[s], (uint32_t)((kc / STAGES) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        float* st = smem + s * STAGE;
+        const uint32_t a_hi = smem_u32(st), b_hi = smem_u32(st + A_ELEMS);
+        const uint32_t a_lo = smem_u32(st + A_ELEMS + B_ELEMS);
+        const uint32_t b_lo = a_lo + A_ELEMS * 4;
 #pragma unroll
-      for (int ks = 0; ks < BK / 8; ++ks) {
-        const uint32_t koff = ks * 2 * 128;  // two core matrices along K per MMA
-        const uint64_t ah = make_desc(smem_u32(a_hi) + koff);
-        const uint64_t bh = make_desc(smem_u32(b_hi) + koff);
-        const uint32_t acc = (kc > 0 || ks > 0) ? 1u : 0u;
-        mma_tf32(tmem, ah, bh, idesc, acc);
-        if (SPLIT) {
-          const uint64_t al = make_desc(smem_u32(a_lo) + koff);
-          const uint64_t bl = make_desc(smem_u32(b_lo) + koff);
-          mma_tf32(tmem, ah, bl, idesc, 1u);
-          mma_tf32(tmem, al, bh, idesc, 1u);
+        for (int ks = 0; ks < BK / 8; ++ks) {
+          const uint32_t koff = ks * 2 * 128;  // two core matrices along K per MMA
+          const uint64_t ah = make_desc(a_hi + koff), bh = make_desc(b_hi + koff);
+          mma_tf32(tmem, ah, bh, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
+          if (SPLIT) {
+            mma_tf32(tmem, ah, make_desc(b_lo + koff), idesc, 1u);
+            mma_tf32(tmem, make_desc(a_lo + koff), bh, idesc, 1u);
+          }
         }
+        mma_commit(&empty_bar[s]);  // stage s may be refilled once these MMAs complete
       }
-      mma_commit(&bars[s]);
+      mma_commit(&done_bar);  // accumulator complete
     }
-  }
-  // wait for the last commit of each used stage
-  if (nk >= 1) {
-    const int s = (nk - 1) & 1;
-    mbar_wait(&bars[s], phase[s]);
-  }
-  if (nk >= 2) {
-    const int s = nk & 1;  // the other stage's last commit (already complete or pending)
-    mbar_wait(&bars[s], phase[s]);
-  }
-  asm volatile("tcgen05.fence::after_thread_sync;");
-  // epilogue: warp w reads TMEM lanes [32w, 32w+32) = tile rows
-  const int row = m0 + warp * 32 + lane;
-  const uint32_t taddr_row = tmem + ((uint32_t)(warp * 32) << 16);
+    __syncwarp();
+  } else {
+    // ---------------- producers
+    const int p = threadIdx.x - 32;
+    const bool vecA = (A.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
+    const bool vecB = (B.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
+    using IOA = StageIO<TA, BM>;
+    using IOB = StageIO<!TB, BN>;
+    float4 ra[IOA::Q], rb[IOB::Q];
+    if (nk > 0) {
+      IOA::gload(p, a, A.ld, m0, M, 0, K, vecA, ra);
+      IOB::gload(p, b, B.ld, n0, N, 0, K, vecB, rb);
+    }
+    for (int kc = 0; kc < nk; ++kc) {
+      const int s = kc % STAGES;
+      if (kc >= STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((kc / STAGES) - 1) & 1));
+      float* st = smem + s * STAGE;
+      IOA::sstore(p, ra, st, st + A_ELEMS + B_ELEMS, SPLIT);
+      IOB::sstore(p, rb, st + A_ELEMS, st + A_ELEMS + B_ELEMS + A_ELEMS, SPLIT);
+      if (kc + 1 < nk) {  // next chunk's loads fly while the MMA consumes this stage
+        IOA::gload(p, a, A.ld, m0, M, (kc + 1) * BK, K, vecA, ra);
+        IOB::gload(p, b, B.ld, n0, N, (kc + 1) * BK, K, vecB, rb);
+      }
+      asm volatile("fence.proxy.async.shared::cta;");  // generic smem writes -> async proxy
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full_bar[s]);
+    }
+    // ---------------- epilogue: TMEM lane group (warp % 4), column half (warp - 1) / 4
+    mbar_wait(&done_bar, 0u);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int lg = warp & 3;
+    const int row = m0 + lg * 32 + lane;
+    const uint32_t taddr_row = tmem + ((uint32_t)(lg * 32) << 16);
+    const int half = (warp - 1) >> 2;
+    constexpr int CH = BN / 2;
 #pragma unroll 1
-  for (int cb = 0; cb < BN; cb += 16) {
-    uint32_t v[16];
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-          "=r"(v[14]), "=r"(v[15])
-        : "r"(taddr_row + cb));
-    asm volatile("tcgen05.wait::ld.sync.aligned;");
-    if (row < M) {
-      float* crow = c + (int64_t)row * C.ld;
+    for (int cb = half * CH; cb < half * CH + CH; cb += 16) {
+      uint32_t v[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+            "=r"(v[14]), "=r"(v[15])
+          : "r"(taddr_row + cb));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+      if (row < M) {
+        float* crow = c + (int64_t)row * C.ld;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int col = n0 + cb + j;
-        if (col < N) crow[col] = accumulate ? crow[col] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+        for (int j = 0; j < 16; ++j) {
+          const int col = n0 + cb + j;
+          if (col < N) crow[col] = accumulate ? crow[col] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+        }
       }
     }
   }
@@ -288,12 +298,11 @@ template <bool TA, bool TB, int BN, int MODE>
 static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
                      Act<float> A, Act<float> B, Act<float> C, bool acc, cudaStream_t st) {
   constexpr int STAGE = (tc::BM * tc::BK + BN * tc::BK) * (MODE == 3 ? 2 : 1);
-  const size_t smem = (size_t)2 * STAGE * sizeof(float);
+  const size_t smem = (size_t)tc::STAGES * STAGE * sizeof(float);
   auto kern = k_gemm_tc<TA, TB, BN, MODE>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   dim3 grid((N + BN - 1) / BN, (M + tc::BM - 1) / tc::BM, n);
-  kern<<<grid, tc::NTHREADS, smem, st>>>(M, N, K, dM, dK, A, B, C, acc ? 1 : 0);
-  ++g_kernel_launches;
+  LAUNCH_NAMED("k_gemm_tc", st, kern<<<grid, tc::NTHREADS, smem, st>>>(M, N, K, dM, dK, A, B, C, acc ? 1 : 0));
   return 0;
 }
 

@@ -412,6 +412,44 @@ def _dist_info():
     return None, 0, 1
 
 
+def worker_ranks(k: int, active, world: int) -> np.ndarray:
+    """Home rank of every worker's partition: the rank that trains it (assign_workers);
+    workers without training nodes still own feature rows and go round-robin."""
+    wr = np.array([w % world for w in range(k)], dtype=np.int64)
+    for r in range(world):
+        for w in assign_workers(active, r, world):
+            wr[w] = r
+    return wr
+
+
+def feature_shard_map(owner: np.ndarray, worker_rank: np.ndarray, world: int):
+    """node -> (rank holding its feature row, row inside that rank's shard).  Rows of a
+    shard are the rank's nodes in ascending id order.  Returns (node_rank, node_row, rows)."""
+    node_rank = worker_rank[np.asarray(owner, dtype=np.int64)].astype(np.int32)
+    node_row = np.empty(len(owner), dtype=np.int32)
+    rows = []
+    for r in range(world):
+        ids = np.flatnonzero(node_rank == r)
+        node_row[ids] = np.arange(len(ids), dtype=np.int32)
+        rows.append(ids)
+    return node_rank, node_row, rows
+
+
+def reduce_epoch_stats(dist, loss_sum, loss_cnt, ledger):
+    """Sum per-worker loss sums / counts and the epoch ledger over ranks.  Each worker
+    lives on exactly one rank, so every entry has a single non-zero contributor and the
+    sums are exact (identical on every rank)."""
+    torch = _torch()
+    dev = ledger.device
+    ls = torch.as_tensor(np.asarray(loss_sum, dtype=np.float64), device=dev)
+    lc = torch.as_tensor(np.asarray(loss_cnt, dtype=np.int64), device=dev)
+    led = ledger.clone()
+    dist.all_reduce(ls)
+    dist.all_reduce(lc)
+    dist.all_reduce(led)
+    return ls.cpu().numpy(), lc.cpu().numpy(), led
+
+
 def assign_workers(active, rank: int, world: int):
     """Workers (partitions) handled by this rank: contiguous blocks of the active list,
     so rank r's workers precede rank r+1's (the reference's worker order)."""
@@ -432,7 +470,7 @@ class Trainer:
 
     def __init__(self, g, partition, model, cfg, *, batch_size, lr, mode, seed,
                  sampler="ladies", subgraph_size=None, optimizer="sgd", dtype=None,
-                 epochs=1, workers=None, ahead=1):
+                 epochs=1, workers=None, ahead=1, shard_features=None):
         torch = _torch()
         if g.features is None or g.labels is None or g.train_mask is None:
             raise ValueError("training needs features, labels and masks")
@@ -484,6 +522,11 @@ class Trainer:
             self.ps = self.dg.acquire(KIND_SAINT, n_slots, self.L, int(subgraph_size), 1)
             _saint_set(self.dg, self.ps, self.all_train, mode != "local")
         self.gcn = self.ps.gcn(self.dims, self.dtype)
+        self._peer_ptrs = []
+        if shard_features is None:
+            shard_features = self.world > 1
+        if shard_features and self.world > 1:
+            self._install_feature_shards()
         td = torch.float32 if self.dtype == "float32" else torch.float64
         sizes = [w.size for w in model.weights]
         self.n_params = int(sum(sizes))
@@ -514,6 +557,31 @@ class Trainer:
         self._bids = np.zeros(n_slots * max(1, batch_size), dtype=np.int64)
         self._len = C.c_int64()
         self._group = []  # (epoch, it) of the sampled-ahead slot groups
+
+    # -- sharded features over NVLink (one process per GPU) ------------------
+    def _install_feature_shards(self):
+        """Each rank keeps the feature rows of its workers' nodes; peers' shards are
+        mapped with CUDA IPC, so the layer-0 gather reads remote S_0 rows directly over
+        NVLink (the exchange the reference only counts, training.py:199)."""
+        wr = worker_ranks(self.k, self.active, self.world)
+        node_rank, node_row, rows = feature_shard_map(self.partition.owner, wr, self.world)
+        mine = self.dg.upload_shard(self.g.features[rows[self.rank]], self.dtype)
+        handle = np.zeros(64, dtype=np.uint8)
+        check(lib.skg_ipc_handle(mine, ptr(handle, C.c_uint8)))
+        handles = [None] * self.world
+        self.dist.all_gather_object(handles, handle.tobytes())
+        ptrs = []
+        for r, hb in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(mine)
+                continue
+            h = np.frombuffer(hb, dtype=np.uint8).copy()
+            p = C.c_uint64()
+            check(lib.skg_ipc_open(ptr(h, C.c_uint8), C.byref(p)))
+            ptrs.append(int(p.value))
+            self._peer_ptrs.append(int(p.value))
+        self.dg.set_feature_shards(ptrs, node_rank, node_row)
+        self.shard_rows = len(rows[self.rank])
 
     # -- host inputs / sampling -------------------------------------------
     def host_inputs(self, epoch, it, group=0):
@@ -613,6 +681,13 @@ class Trainer:
             w[...] = v.double().cpu().numpy()
 
     def close(self):
+        for p in self._peer_ptrs:
+            lib.skg_ipc_close(p)
+        self._peer_ptrs = []
+        if self.world > 1:  # restore the single-store map for later single-rank use
+            X = self.g.features
+            self.dg.feat_key = None
+            self.dg.ensure_features(X, self.dtype)
         self.dg.release(self.ps)
 
 
@@ -648,12 +723,7 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
                 loss_sum[w] += losses[j, i]
                 loss_cnt[w] += 1
         if tr.world > 1:
-            ls = torch.as_tensor(loss_sum, device="cuda")
-            lc = torch.as_tensor(loss_cnt, device="cuda")
-            tr.dist.all_reduce(ls)
-            tr.dist.all_reduce(lc)
-            tr.dist.all_reduce(ledger)
-            loss_sum, loss_cnt = ls.cpu().numpy(), lc.cpu().numpy()
+            loss_sum, loss_cnt, ledger = reduce_epoch_stats(tr.dist, loss_sum, loss_cnt, ledger)
         ledger_np = ledger.cpu().numpy()
         logits = _predict_device(tr.dg, tr.wviews, tr.dims, tr.dtype)
         preds = torch.argmax(logits, dim=1)
