@@ -49,7 +49,6 @@ using namespace skg;
     }                        \
   } while (0)
 
-static inline int64_t round4(int64_t d) { return (d + 3) / 4 * 4; }
 
 // ------------------------------------------------------------------ structures
 struct skg_ctx {
@@ -144,6 +143,11 @@ struct skg_gcn {
   std::vector<char*> U, H;
   char* G0 = nullptr;
   char* G1 = nullptr;
+  // TF32 lo parts of the tensor-core GEMM operands (fp32 only): U_l, G, and the weights'
+  // padded hi / lo copies (row stride ldw[l] = round4(d_{l+1}))
+  std::vector<char*> Ulo, Wh, Wl;
+  std::vector<int64_t> ldw;
+  char* G0lo = nullptr;
   char* parts = nullptr;  // split-K partials of dW, one d_l x d_{l+1} block per slot
   int64_t part_elems = 0;
   double* row_loss = nullptr;
@@ -1010,6 +1014,19 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   for (int l = 1; l <= L; ++l) cv.add(g->H[l], (size_t)S * R * g->ld[l] * es);
   cv.add(g->G0, (size_t)S * R * g->ld_max * es);
   cv.add(g->G1, (size_t)S * R * g->ld_max * es);
+  if (dtype == DT_F32) {
+    g->Ulo.resize(L);
+    g->Wh.resize(L);
+    g->Wl.resize(L);
+    g->ldw.resize(L);
+    for (int l = 0; l < L; ++l) {
+      cv.add(g->Ulo[l], (size_t)S * R * g->ld[l] * es);
+      g->ldw[l] = round4(dims[l + 1]);
+      cv.add(g->Wh[l], (size_t)dims[l] * g->ldw[l] * es);
+      cv.add(g->Wl[l], (size_t)dims[l] * g->ldw[l] * es);
+    }
+    cv.add(g->G0lo, (size_t)S * R * g->ld_max * es);
+  }
   cv.add(g->parts, (size_t)S * wmax * es);
   cv.add(g->row_loss, (size_t)S * R);
   cv.add(g->d_layers, (size_t)L * S);
@@ -1094,6 +1111,10 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
   const int Ri = (int)R;
   int rc = refresh_batches(g, z0, n, st);
   if (rc) return rc;
+  // fp32 GEMMs on tcgen05 (mode 1 / 3) read TF32-split operands; 3xTF32 also needs lo parts
+  constexpr bool F32 = sizeof(T) == 4;
+  const int mode = F32 ? g_gemm_mode : 0;
+  const bool tc = mode != 0, split = mode == 3;
   auto W = [&](int l) {
     Act<T> a;
     a.base = reinterpret_cast<T*>(wp[l]);
@@ -1101,22 +1122,66 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     a.ld = g->dims[l + 1];
     return a;
   };
+  auto lo_of = [&](char* base, int64_t ld_alloc) -> T* {
+    return split ? reinterpret_cast<T*>(base) + (int64_t)z0 * R * ld_alloc : nullptr;
+  };
+  auto op = [&](char* hi, char* lo, int64_t ld_alloc, int64_t ld) {
+    TcOp o;
+    o.hi = reinterpret_cast<const float*>(hi) + (int64_t)z0 * R * ld_alloc;
+    o.lo = split ? reinterpret_cast<const float*>(lo) + (int64_t)z0 * R * ld_alloc : nullptr;
+    o.ld = ld;
+    o.stride = R * ld_alloc;
+    o.rows_cap = R;
+    return o;
+  };
+  auto wop = [&](int l) {
+    TcOp o;
+    o.hi = reinterpret_cast<const float*>(g->Wh[l]);
+    o.lo = split ? reinterpret_cast<const float*>(g->Wl[l]) : nullptr;
+    o.ld = g->ldw[l];
+    o.stride = 0;
+    o.rows_cap = g->dims[l];
+    return o;
+  };
+  if (tc) {
+    WSplitTable t;
+    t.L = L;
+    for (int l = 0; l < L; ++l) {
+      t.w[l] = reinterpret_cast<const float*>(wp[l]);
+      t.hi[l] = reinterpret_cast<float*>(g->Wh[l]);
+      t.lo[l] = split ? reinterpret_cast<float*>(g->Wl[l]) : nullptr;
+      t.rows[l] = g->dims[l];
+      t.cols[l] = g->dims[l + 1];
+      t.ld_out[l] = g->ldw[l];
+    }
+    split_weights(t, st);
+  }
   Act<T> X0 = act<T>(g->X0, R, g->ld[0], g->ld[0], z0);
   gather_rows_b<T>(c->fstore(), g->d_slots + z0, n, Ri, X0, st);
   for (int l = 0; l < L; ++l) {
     const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
+    const int32_t* const* rows = g->d_rows + (size_t)l * S + z0;
     Act<T> A = l == 0 ? X0 : act<T>(g->H[l], R, g->ld[l], g->ld[l], z0);
     Act<T> U = act<T>(g->U[l], R, g->ld[l], g->ld[l], z0);
-    spmm_b<T>(lds, n, Ri, false, l > 0, A, A, U, g->ld[l], st);
+    spmm_b<T>(lds, n, Ri, false, l > 0, A, A, U, F32 ? lo_of(g->Ulo[l], g->ld[l]) : nullptr, g->ld[l], st);
     Act<T> Hn = act<T>(g->H[l + 1], R, g->ld[l + 1], g->ld[l + 1], z0);
-    gemm_b<T>(false, false, n, Ri, (int)g->dims[l + 1], (int)g->dims[l],
-              g->d_rows + (size_t)l * S + z0, nullptr, U, W(l), Hn, false, st);
+    if constexpr (F32) {
+      if (tc) {
+        rc = gemm_tc(mode, false, false, n, Ri, (int)g->dims[l + 1], (int)g->dims[l], rows, nullptr,
+                     op(g->U[l], g->Ulo[l], g->ld[l], g->ld[l]), wop(l), Hn, false, st);
+        if (rc) return rc;
+        continue;
+      }
+    }
+    gemm_simt<T>(false, false, n, Ri, (int)g->dims[l + 1], (int)g->dims[l], rows, nullptr, U, W(l), Hn,
+                 false, st);
   }
   if (!backward) return SKG_OK;
   Act<T> G = act<T>(g->G0, R, g->ld_max, g->ld[L], z0);
   Act<T> Gu = act<T>(g->G1, R, g->ld_max, g->ld[L], z0);
+  T* G_lo = F32 ? lo_of(g->G0lo, g->ld_max) : nullptr;
   softmax_ce_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
-                  (int)g->dims[L], G, g->row_loss + (size_t)z0 * R, loss, st);
+                  (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, loss, st);
   for (int l = L - 1; l >= 0; --l) {
     const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
     const int32_t* const* rows = g->d_rows + (size_t)l * S + z0;
@@ -1126,16 +1191,35 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     P.base = reinterpret_cast<T*>(g->parts);
     P.stride = g->part_elems;
     P.ld = dn;
-    gemm_b<T>(true, false, n, dl, dn, Ri, nullptr, rows, act<T>(g->U[l], R, g->ld[l], g->ld[l], z0), G,
-              P, false, st);
+    bool done = false;
+    if constexpr (F32) {
+      if (tc) {
+        rc = gemm_tc(mode, true, false, n, dl, dn, Ri, nullptr, rows, op(g->U[l], g->Ulo[l], g->ld[l], g->ld[l]),
+                     op(g->G0, g->G0lo, g->ld_max, G.ld), P, false, st);
+        if (rc) return rc;
+        done = true;
+      }
+    }
+    if (!done)
+      gemm_simt<T>(true, false, n, dl, dn, Ri, nullptr, rows, act<T>(g->U[l], R, g->ld[l], g->ld[l], z0), G,
+                   P, false, st);
     reduce_slots<T>(P.base, P.stride, n, dl, dn, dn, reinterpret_cast<T*>(gp[l]), dn, accum, st);
     if (l == 0) break;
     // G_u = G W_l^T ; G <- (Block_l^T G_u) * [H_l > 0]
     Gu.ld = g->ld[l];
-    gemm_b<T>(false, true, n, Ri, dl, dn, rows, nullptr, G, W(l), Gu, false, st);
+    done = false;
+    if constexpr (F32) {
+      if (tc) {
+        rc = gemm_tc(mode, false, true, n, Ri, dl, dn, rows, nullptr, op(g->G0, g->G0lo, g->ld_max, G.ld), wop(l),
+                     Gu, false, st);
+        if (rc) return rc;
+        done = true;
+      }
+    }
+    if (!done) gemm_simt<T>(false, true, n, Ri, dl, dn, rows, nullptr, G, W(l), Gu, false, st);
     Act<T> Gn = G;
     Gn.ld = g->ld[l];
-    spmm_b<T>(lds, n, Ri, true, false, Gu, act<T>(g->H[l], R, g->ld[l], g->ld[l], z0), Gn,
+    spmm_b<T>(lds, n, Ri, true, false, Gu, act<T>(g->H[l], R, g->ld[l], g->ld[l], z0), Gn, G_lo,
               g->ld[l], st);
     G = Gn;
   }
@@ -1210,10 +1294,19 @@ extern "C" int skg_predict_logits(skg_ctx* c, int L, const int64_t* dims, const 
   const size_t es = dtype == DT_F32 ? 4 : 8;
   int64_t ldm = 0;
   for (int l = 0; l <= L; ++l) ldm = std::max(ldm, round4(dims[l]));
-  char *U = nullptr, *H = nullptr;
+  char *U = nullptr, *H = nullptr, *Ul = nullptr, *Wh = nullptr, *Wl = nullptr;
+  const int mode = dtype == DT_F32 ? g_gemm_mode : 0;  // fp32: tcgen05 on TF32-split operands
+  int64_t wmax = 0;
+  for (int l = 0; l < L; ++l) wmax = std::max(wmax, dims[l] * round4(dims[l + 1]));
   CK(cudaMalloc(&U, es * ldm * std::max<int64_t>(c->n, 1)));
   CK(cudaMalloc(&H, es * ldm * std::max<int64_t>(c->n, 1)));
   CK(cudaMemsetAsync(H, 0, es * ldm * std::max<int64_t>(c->n, 1), st));
+  if (mode) {
+    CK(cudaMalloc(&Ul, es * ldm * std::max<int64_t>(c->n, 1)));
+    CK(cudaMalloc(&Wh, es * std::max<int64_t>(wmax, 1)));
+    CK(cudaMalloc(&Wl, es * std::max<int64_t>(wmax, 1)));
+  }
+  int rc = SKG_OK;
   for (int l = 0; l < L; ++l) {
     const int64_t ldi = l == 0 ? c->ldx : round4(dims[l]);
     const int64_t ldl = round4(dims[l]);
@@ -1222,8 +1315,23 @@ extern "C" int skg_predict_logits(skg_ctx* c, int L, const int64_t* dims, const 
     if (dtype == DT_F32) {
       const float* A = l == 0 ? (const float*)c->d_x : (const float*)H;
       spmm_full<float>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (float*)U, ldl, ldl, st);
-      gemm_plain<float>((int)c->n, (int)dims[l + 1], (int)dims[l], (const float*)U, ldl,
-                        (const float*)wp[l], dims[l + 1], last ? (float*)out_dev : (float*)H, ldo, st);
+      if (mode) {
+        // P·(X·W) rounding differs from the fp64 reference only at fp32 level (3xTF32)
+        float* uh = (float*)U;
+        float* ul = mode == 3 ? (float*)Ul : nullptr;
+        split_tf32(uh, ldl, c->n, dims[l], uh, ul, ldl, st);  // in place: hi over U
+        const int64_t ldw = round4(dims[l + 1]);
+        split_tf32((const float*)wp[l], dims[l + 1], dims[l], dims[l + 1], (float*)Wh,
+                   mode == 3 ? (float*)Wl : nullptr, ldw, st);
+        TcOp a{uh, ul, ldl, 0, c->n}, b{(const float*)Wh, mode == 3 ? (const float*)Wl : nullptr, ldw, 0, dims[l]};
+        Act<float> out{last ? (float*)out_dev : (float*)H, 0, ldo};
+        rc = gemm_tc(mode, false, false, 1, (int)c->n, (int)dims[l + 1], (int)dims[l], nullptr, nullptr, a, b,
+                     out, false, st);
+        if (rc) break;
+      } else {
+        gemm_plain<float>((int)c->n, (int)dims[l + 1], (int)dims[l], (const float*)U, ldl,
+                          (const float*)wp[l], dims[l + 1], last ? (float*)out_dev : (float*)H, ldo, st);
+      }
     } else {
       const double* A = l == 0 ? (const double*)c->d_x : (const double*)H;
       spmm_full<double>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (double*)U, ldl, ldl, st);
@@ -1232,9 +1340,13 @@ extern "C" int skg_predict_logits(skg_ctx* c, int L, const int64_t* dims, const 
                          st);
     }
   }
-  CK(cudaStreamSynchronize(st));
+  cudaStreamSynchronize(st);
   cudaFree(U);
   cudaFree(H);
+  if (Ul) cudaFree(Ul);
+  if (Wh) cudaFree(Wh);
+  if (Wl) cudaFree(Wl);
+  if (rc) return rc;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("predict_logits: ") + cudaGetErrorString(e));

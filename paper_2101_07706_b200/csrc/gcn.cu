@@ -100,8 +100,21 @@ void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows,
 }
 
 // ------------------------------------------------------------------ SpMM (K8 / K10)
+// TF32 split of a result vector for the tensor-core GEMMs: hi into o, lo into o_lo
+__device__ __forceinline__ void store_split(const Vec4<float>& a, float* o, float* o_lo) {
+  float4 h, l;
+  h.x = tf32_rna(a.v.x); l.x = tf32_rna(a.v.x - h.x);
+  h.y = tf32_rna(a.v.y); l.y = tf32_rna(a.v.y - h.y);
+  h.z = tf32_rna(a.v.z); l.z = tf32_rna(a.v.z - h.z);
+  h.w = tf32_rna(a.v.w); l.w = tf32_rna(a.v.w - h.w);
+  *reinterpret_cast<float4*>(o) = h;
+  *reinterpret_cast<float4*>(o_lo) = l;
+}
+__device__ __forceinline__ void store_split(const Vec4<double>&, double*, double*) {}
+
 template <typename T, bool TRANS, bool RELU>
-__global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, int64_t width) {
+__global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, T* out_lo,
+                         int max_rows, int64_t width) {
   const LayerDesc d = lds[blockIdx.y];
   const int rows = TRANS ? *d.cols : *d.rows;
   const int32_t* __restrict__ ip = TRANS ? d.tindptr : d.indptr;
@@ -110,9 +123,19 @@ __global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, i
   const T* a = A.at(blockIdx.y);
   const T* h = TRANS ? H.at(blockIdx.y) : nullptr;
   T* o = out.at(blockIdx.y);
+  T* ol = out_lo ? out_lo + (int64_t)blockIdx.y * out.stride : nullptr;
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
+  // split outputs feed the GEMM's contraction over rows: rows past the plan's are zero
+  const int rows_all = ol ? max_rows : rows;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows_all; r += nw) {
+    if (r >= rows) {
+      for (int64_t c = lane * 4; c < width; c += 128) {
+        Vec4<T>::zero().store(o + (int64_t)r * out.ld + c);
+        Vec4<T>::zero().store(ol + (int64_t)r * out.ld + c);
+      }
+      continue;
+    }
     const int b = ip[r], e = ip[r + 1];
     for (int64_t c = lane * 4; c < width; c += 128) {
       Vec4<T> acc = Vec4<T>::zero();
@@ -122,18 +145,19 @@ __global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, i
         acc.fma((T)vv[p], x);
       }
       if (TRANS) acc.mask(Vec4<T>::load(h + (int64_t)r * H.ld + c));
-      acc.store(o + (int64_t)r * out.ld + c);
+      if (ol) store_split(acc, o + (int64_t)r * out.ld + c, ol + (int64_t)r * out.ld + c);
+      else acc.store(o + (int64_t)r * out.ld + c);
     }
   }
 }
 
 template <typename T>
 void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
-            Act<T> H, Act<T> out, int64_t width, cudaStream_t st) {
+            Act<T> H, Act<T> out, T* out_lo, int64_t width, cudaStream_t st) {
   dim3 grid(row_blocks(max_rows, n), n);
-  if (transposed) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, true, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
-  else if (relu_in) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, true><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
-  else LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, false><<<grid, 256, 0, st>>>(ld, A, H, out, width)));
+  if (transposed) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, true, false><<<grid, 256, 0, st>>>(ld, A, H, out, out_lo, max_rows, width)));
+  else if (relu_in) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, true><<<grid, 256, 0, st>>>(ld, A, H, out, out_lo, max_rows, width)));
+  else LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, false><<<grid, 256, 0, st>>>(ld, A, H, out, out_lo, max_rows, width)));
 }
 
 // full-graph SpMM for predict_logits (int64 offsets)
@@ -255,21 +279,12 @@ static void gemm_launch(bool ta, bool tb, int n, int M, int N, int K, const int3
 }
 
 int g_gemm_mode = 3;  // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
-int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
-            const int32_t* const* dK, Act<float> A, Act<float> B, Act<float> C, bool acc,
-            cudaStream_t st);
 
 template <typename T>
-void gemm_b(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
-            const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool accumulate,
-            cudaStream_t st) {
+void gemm_simt(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+               const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool accumulate,
+               cudaStream_t st) {
   if (M <= 0 || N <= 0 || n <= 0) return;
-  if constexpr (sizeof(T) == 4) {
-    if (g_gemm_mode != 0) {
-      gemm_tc(g_gemm_mode, ta, tb, n, M, N, K, dM, dK, A, B, C, accumulate, st);
-      return;
-    }
-  }
   if (sizeof(T) == 4 && N > 32)
     gemm_launch<T, 128, 64, 16, 8, 4>(ta, tb, n, M, N, K, dM, dK, A, B, C, accumulate, st);
   else
@@ -286,7 +301,7 @@ void gemm_plain(int M, int N, int K, const T* A, int64_t lda, const T* B, int64_
     Act<T> a2 = a, c2 = c;
     a2.base += (int64_t)m0 * lda;
     c2.base += (int64_t)m0 * ldc;
-    gemm_b<T>(false, false, 1, std::min(chunk, M - m0), N, K, nullptr, nullptr, a2, b, c2, false, st);
+    gemm_simt<T>(false, false, 1, std::min(chunk, M - m0), N, K, nullptr, nullptr, a2, b, c2, false, st);
   }
 }
 
@@ -318,7 +333,7 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
 // fixed-order per-slot mean.
 template <typename T>
 __global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T> Z, int C,
-                               Act<T> G, double* row_loss, int64_t rl_stride) {
+                               Act<T> G, T* G_lo, int max_rows, double* row_loss, int64_t rl_stride) {
   const SlotDesc d = sd[blockIdx.y];
   const int n = *d.n_batch;
   __shared__ int s_nlab;
@@ -332,14 +347,24 @@ __global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T>
   const int nlab = s_nlab;
   const T* z0 = Z.at(blockIdx.y);
   T* g0 = G.at(blockIdx.y);
+  T* gl0 = G_lo ? G_lo + (int64_t)blockIdx.y * G.stride : nullptr;
   double* rl = row_loss + blockIdx.y * rl_stride;
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
-    const int y = labels[d.batch[r]];
+  const int rows_all = gl0 ? max_rows : n;  // split output: zero rows past the batch
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows_all; r += nw) {
     T* g = g0 + (int64_t)r * G.ld;
+    T* gl = gl0 ? gl0 + (int64_t)r * G.ld : nullptr;
+    if (r >= n) {
+      for (int k = lane; k < C; k += 32) g[k] = gl[k] = T(0);
+      continue;
+    }
+    const int y = labels[d.batch[r]];
     if (y < 0 || nlab == 0) {
-      for (int k = lane; k < C; k += 32) g[k] = T(0);
+      for (int k = lane; k < C; k += 32) {
+        g[k] = T(0);
+        if (gl) gl[k] = T(0);
+      }
       if (lane == 0) rl[r] = 0.0;
       continue;
     }
@@ -355,7 +380,14 @@ __global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T>
     const double lse = zmax + log(se);
     for (int k = lane; k < C; k += 32) {
       double gz = exp((double)z[k] - lse) - (k == y ? 1.0 : 0.0);
-      g[k] = (T)(gz / nlab);
+      const T v = (T)(gz / nlab);
+      if (gl) {
+        const float h = tf32_rna((float)v);
+        g[k] = (T)h;
+        gl[k] = (T)tf32_rna((float)v - h);
+      } else {
+        g[k] = v;
+      }
     }
     if (lane == 0) rl[r] = lse - (double)z[y];
   }
@@ -388,9 +420,9 @@ __global__ void k_loss_mean(const SlotDesc* sd, const int32_t* labels, const dou
 
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
-                  Act<T> G, double* row_loss, double* loss_out, cudaStream_t st) {
+                  Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st) {
   LAUNCH_NAMED("k_softmax_ce_b", st, (k_softmax_ce_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(
-      sd, labels, Z, C, G, row_loss, max_rows)));
+      sd, labels, Z, C, G, G_lo, max_rows, row_loss, max_rows)));
   LAUNCH_NAMED("k_loss_mean", st, (k_loss_mean<<<n, 256, 0, st>>>(sd, labels, row_loss, max_rows, loss_out)));
 }
 
@@ -458,13 +490,13 @@ void fill_zero(T* p, int64_t n, cudaStream_t st) {
 
 #define INST(T)                                                                                     \
   template void gather_rows_b<T>(const FeatStore&, const SlotDesc*, int, int, Act<T>, cudaStream_t); \
-  template void spmm_b<T>(const LayerDesc*, int, int, bool, bool, Act<T>, Act<T>, Act<T>, int64_t,  \
-                          cudaStream_t);                                                            \
-  template void gemm_b<T>(bool, bool, int, int, int, int, const int32_t* const*,                    \
-                          const int32_t* const*, Act<T>, Act<T>, Act<T>, bool, cudaStream_t);       \
+  template void spmm_b<T>(const LayerDesc*, int, int, bool, bool, Act<T>, Act<T>, Act<T>, T*,       \
+                          int64_t, cudaStream_t);                                                   \
+  template void gemm_simt<T>(bool, bool, int, int, int, int, const int32_t* const*,                 \
+                             const int32_t* const*, Act<T>, Act<T>, Act<T>, bool, cudaStream_t);    \
   template void reduce_slots<T>(const T*, int64_t, int, int64_t, int64_t, int64_t, T*, int64_t,     \
                                 bool, cudaStream_t);                                                \
-  template void softmax_ce_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>,     \
+  template void softmax_ce_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>, T*, \
                                 double*, double*, cudaStream_t);                                    \
   template void sgd_step<T>(T*, const T*, int64_t, double, double, cudaStream_t);                   \
   template void adam_step<T>(T*, const T*, T*, T*, int64_t, double, double, double, double, double, \

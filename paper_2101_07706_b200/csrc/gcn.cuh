@@ -46,25 +46,63 @@ struct Act {
   __host__ __device__ T* at(int z) const { return base + (int64_t)z * stride; }
 };
 
+// A GEMM operand for the tensor-core path: TF32 hi / lo parts (lo null for 1xTF32) with
+// identical geometry, rows of ld elements (ld % 4 == 0), slot z at + z*stride (stride 0:
+// shared by all slots), rows_cap rows allocated per slot.
+struct TcOp {
+  const float* hi;
+  const float* lo;
+  int64_t ld, stride, rows_cap;
+};
+
+constexpr int kMaxLayers = 16;
+// weights of every layer -> padded TF32 hi / lo copies (k_split_weights)
+struct WSplitTable {
+  int L;
+  const float* w[kMaxLayers];
+  float* hi[kMaxLayers];
+  float* lo[kMaxLayers];
+  int64_t rows[kMaxLayers], cols[kMaxLayers], ld_out[kMaxLayers];
+};
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+extern int g_gemm_mode;  // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
+// C_z = op(A_z) op(B_z) (+ C_z) on tcgen05 (TMA-fed); M (or K) per slot from dM / dK
+int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+            const int32_t* const* dK, const TcOp& A, const TcOp& B, Act<float> C, bool acc,
+            cudaStream_t st);
+void split_tf32(const float* in, int64_t ld_in, int64_t rows, int64_t cols, float* hi, float* lo,
+                int64_t ld_out, cudaStream_t st);
+void split_weights(const WSplitTable& t, cudaStream_t st);
+
 template <typename T>
 void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows, Act<T> out,
                    cudaStream_t st);
-// out = Block_l (relu?(A))  or, transposed, out = (Block_l^T A) * [H > 0]
+// out = Block_l (relu?(A))  or, transposed, out = (Block_l^T A) * [H > 0].
+// With out_lo (fp32 only) the result is written TF32-split (hi into out, lo into out_lo)
+// for the tensor-core GEMMs, and rows [rows, max_rows) of every slot are zeroed.
 template <typename T>
 void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
-            Act<T> H, Act<T> out, int64_t width, cudaStream_t st);
-// C_z = op(A_z) op(B_z) (+ C_z).  M (or K) per slot from device scalars rows[z] when given.
+            Act<T> H, Act<T> out, T* out_lo, int64_t width, cudaStream_t st);
+// SIMT GEMM (fp64, and the fp32 fallback mode 0): C_z = op(A_z) op(B_z) (+ C_z).
+// M (or K) per slot from device scalars rows[z] when given.
 template <typename T>
-void gemm_b(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
-            const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool accumulate,
-            cudaStream_t st);
+void gemm_simt(bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
+               const int32_t* const* dK, Act<T> A, Act<T> B, Act<T> C, bool accumulate,
+               cudaStream_t st);
 // C (+)= sum_z P_z in slot order (deterministic split-K reduction)
 template <typename T>
 void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int64_t cols,
                   int64_t ldp, T* C, int64_t ldc, bool accumulate, cudaStream_t st);
+// G (and G_lo when given: TF32-split output, rows [n_batch, max_rows) zeroed)
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
-                  Act<T> G, double* row_loss, double* loss_out, cudaStream_t st);
+                  Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st);
 template <typename T>
 void sgd_step(T* w, const T* g, int64_t n, double lr, double contrib, cudaStream_t st);
 template <typename T>

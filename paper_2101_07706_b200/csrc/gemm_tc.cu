@@ -1,20 +1,36 @@
 // tcgen05 (5th-gen tensor core) GEMM for the GCN's dense contractions H·W, G·Wᵀ, Uᵀ·G.
 //
-// Warp-specialised, one 128 x BN output tile per CTA, fp32 accumulator in TMEM:
-//   warp 0      : TMEM allocation; lane 0 issues tcgen05.mma.kind::tf32 for every K step of
-//                 a full stage and commits it to that stage's "empty" mbarrier
-//   warps 1..8  : producers.  They read operands from global memory (any transposition),
-//                 split them into TF32 hi/lo parts and write the canonical no-swizzle
-//                 K-major UMMA layout (8-row x 16-byte core matrices; LBO = next core matrix
-//                 along K, SBO = next along M/N) into a STAGES-deep shared-memory ring, then
-//                 arrive on the stage's "full" mbarrier.  The next chunk's global loads are
-//                 issued before the current chunk is converted (register double buffer).
-//                 After the last commit they drain TMEM (tcgen05.ld) into global memory.
-//   MODE 1: 1xTF32 (10-bit mantissa inputs)
-//   MODE 3: 3xTF32  D += Ahi Bhi + Ahi Blo + Alo Bhi  (~fp32 accuracy; default, keeps the
-//           rtol 1e-4 parity of fp32 activations/gradients against the fp64 reference)
+// Operands arrive pre-split into TF32 hi / lo fp32 arrays (the producing kernels write
+// them: SpMM -> U, softmax / transposed SpMM -> G, k_split_weights -> W), so this kernel is
+// a pure TMA -> tcgen05 pipeline:
+//   warp 0 (one lane) : TMA producer.  Per 32-wide K chunk it loads the hi (and lo) boxes of
+//                       A and B into one stage of a STAGES-deep ring (SWIZZLE_128B) and
+//                       arms the stage's "full" mbarrier with the byte count.
+//   warp 1 (one lane) : TMEM allocation + MMA issuer: tcgen05.mma.kind::tf32, 128 x BN x 8,
+//                       3 per K step for 3xTF32 (Ahi·Bhi + Ahi·Blo + Alo·Bhi, ~fp32
+//                       accuracy) or 1 for 1xTF32; tcgen05.commit frees the stage.
+//   warps 2..5        : epilogue: tcgen05.ld of their TMEM lane quarter -> global (float4).
+// Operand layouts in shared memory (both supported by the MMA, checked by
+// tools/mn_probe.cu):
+//   K-major  (operand contiguous along K):  one TMA box {32 k, rows}; 8-row x 128-byte
+//            swizzle atoms, SBO = 1024 B; a K = 8 step advances the start by 32 B.
+//   MN-major (operand contiguous along M/N, i.e. a transposed operand): boxes {32 mn, 32 k}
+//            of 4 KB side by side (LBO = 4096 B) in the SW128_32B layout, the only one tf32
+//            allows for MN-major (TMA SWIZZLE_128B_ATOM_32B; 4 k-rows x 128 B atoms, SBO =
+//            512 B); a K = 8 step is 8 rows = 1024 B.
+// The slot (plan) index is the third tensor-map dimension; per-slot M or K comes from
+// device scalars.  Rows of a slot beyond its K are zero in the producers' buffers, so the
+// contraction over a slot's rows needs no masking; rows beyond M are masked at the store.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <unordered_map>
 
 #include "gcn.cuh"
 #include "prof.h"
@@ -26,42 +42,29 @@ namespace skg {
 namespace tc {
 
 constexpr int BM = 128;
-constexpr int BK = 32;                 // K elements per stage (4 MMAs of K = 8)
-constexpr int KGROUPS = BK / 4;        // core matrices along K per stage
-constexpr int NPROD = 256;             // producer threads (8 warps)
-constexpr int NTHREADS = 32 + NPROD;
-constexpr int STAGES = 4;
+constexpr int BK = 32;         // K elements per stage (4 MMAs of K = 8)
+constexpr int NTHREADS = 192;  // TMA warp, MMA warp, 4 epilogue warps
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// canonical K-major, no swizzle: element (row, k) of a tile
-__device__ __forceinline__ int kmaj_off(int row, int k) {
-  return (((row >> 3) * KGROUPS + (k >> 2)) << 5) + ((row & 7) << 2) + (k & 3);
-}
-
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
-  const uint64_t lbo = 128, sbo = (uint64_t)KGROUPS * 128;
+// layout: 2 = SWIZZLE_128B (K-major), 1 = SWIZZLE_128B_BASE32B (MN-major tf32)
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-  return d;                // base offset 0, legacy LBO mode, SWIZZLE_NONE
+  d |= (uint64_t)layout << 61;
+  return d;
 }
 
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
-  // c_format F32 (bit 4), a/b format TF32 (=2 at bits 7, 10), K-major A and B,
-  // n_dim = N >> 3 at bit 17, m_dim = M >> 4 at bit 24
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ float to_tf32(float x) {
-  uint32_t r;
-  asm volatile("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
+  // c_format F32 (bit 4), a/b format TF32 (=2 at bits 7, 10), a/b major (bits 15/16,
+  // 1 = MN-major), n_dim = N >> 3 at bit 17, m_dim = M >> 4 at bit 24
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
@@ -80,8 +83,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity));
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)));
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+
+__device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
 }
 
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
@@ -100,107 +111,61 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       smem_u32(bar)));
 }
 
-// Each quad is 4 consecutive k of one tile row, stored as one 16-byte smem write.  The 8
-// lanes of a warp sharing a k group cover the 8 rows of one core matrix (a full 128-byte
-// smem row: conflict-free) and global reads stay coalesced (TRANS: lanes walk the
-// contiguous row axis).
-template <bool TRANS, int ROWS>
-struct StageIO {
-  static constexpr int Q = ROWS * BK / 4 / NPROD;  // float4 quads per producer thread
-  __device__ static void coords(int p, int q, int& r, int& k) {
-    const int qd = p + q * NPROD;
-    if (TRANS) {
-      r = qd % ROWS;
-      k = (qd / ROWS) * 4;
-    } else {
-      r = (qd & 7) + 8 * (qd >> 6);
-      k = ((qd >> 3) & 7) * 4;
-    }
-  }
-  // tile element (r, k) = TRANS ? src[(k0+k)*ld + row0 + r] : src[(row0+r)*ld + k0 + k]
-  __device__ static void gload(int p, const float* __restrict__ src, int64_t ld, int row0,
-                               int nrows, int k0, int K, bool vec, float4 (&v)[Q]) {
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      int r, k;
-      coords(p, q, r, k);
-      const int gr = row0 + r, gk = k0 + k;
-      float t[4];
-      if (TRANS) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          t[e] = (gr < nrows && gk + e < K) ? __ldg(src + (int64_t)(gk + e) * ld + gr) : 0.f;
-      } else {
-        if (vec && gr < nrows && gk + 3 < K) {
-          v[q] = __ldg(reinterpret_cast<const float4*>(src + (int64_t)gr * ld + gk));
-          continue;
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e)
-          t[e] = (gr < nrows && gk + e < K) ? __ldg(src + (int64_t)gr * ld + gk + e) : 0.f;
-      }
-      v[q] = make_float4(t[0], t[1], t[2], t[3]);
-    }
-  }
-  __device__ static void sstore(int p, const float4 (&v)[Q], float* s_hi, float* s_lo, bool split) {
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      int r, k;
-      coords(p, q, r, k);
-      const float x[4] = {v[q].x, v[q].y, v[q].z, v[q].w};
-      float hi[4], lo[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        hi[e] = to_tf32(x[e]);
-        lo[e] = to_tf32(x[e] - hi[e]);
-      }
-      const int o = kmaj_off(r, k);
-      *reinterpret_cast<float4*>(s_hi + o) = make_float4(hi[0], hi[1], hi[2], hi[3]);
-      if (split) *reinterpret_cast<float4*>(s_lo + o) = make_float4(lo[0], lo[1], lo[2], lo[3]);
-    }
-  }
+template <int BN, int MODE>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4, B_BYTES = BN * BK * 4;
+  static constexpr int PARTS = MODE == 3 ? 2 : 1;
+  static constexpr int STAGE = (A_BYTES + B_BYTES) * PARTS;
+  static constexpr int STAGES_FIT = (200 * 1024) / STAGE;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE + 1024;  // + 1 KB alignment slack
 };
 
 }  // namespace tc
 
+struct TcMaps {
+  CUtensorMap a_hi, a_lo, b_hi, b_lo;
+};
+
 // C_z = op(A_z) op(B_z) (+ C_z) on tensor cores; op(A) M x K, op(B) K x N.
+// TA: A stored K x M (contiguous along M); TB: B stored N x K (contiguous along K).
 template <bool TA, bool TB, int BN, int MODE>
 __global__ void __launch_bounds__(tc::NTHREADS, 1)
-    k_gemm_tc(int Mfix, int N, int Kfix, const int32_t* const* dM, const int32_t* const* dK,
-              Act<float> A, Act<float> B, Act<float> C, int accumulate) {
+    k_gemm_tc(const __grid_constant__ TcMaps maps, int Mfix, int N, int Kfix,
+              const int32_t* const* dM, const int32_t* const* dK, int a_slots, int b_slots,
+              Act<float> C, int accumulate) {
   using namespace tc;
+  using CF = Cfg<BN, MODE>;
   constexpr bool SPLIT = MODE == 3;
-  constexpr int A_ELEMS = BM * BK, B_ELEMS = BN * BK;
-  constexpr int STAGE = (A_ELEMS + B_ELEMS) * (SPLIT ? 2 : 1);
+  constexpr int STAGES = CF::STAGES;
   constexpr int TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  extern __shared__ __align__(1024) float smem[];
+  constexpr bool A_MN = TA, B_MN = !TB;
+  extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], done_bar;
   __shared__ uint32_t tmem_base;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
   const int z = blockIdx.z;
   const int M = dM ? *dM[z] : Mfix;
   const int K = dK ? *dK[z] : Kfix;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   if (m0 >= M) return;
-  const float* __restrict__ a = A.at(z);
-  const float* __restrict__ b = B.at(z);
-  float* __restrict__ c = C.at(z);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = (K + BK - 1) / BK;
+  const int nk = K > 0 ? (K + BK - 1) / BK : 0;
 
-  if (warp == 0) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_base)),
                  "n"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    if (lane == 0) {
-      for (int s = 0; s < STAGES; ++s) {
-        mbar_init(&full_bar[s], NPROD / 32);  // one arrive per producer warp
-        mbar_init(&empty_bar[s], 1);          // tcgen05.commit
-      }
-      mbar_init(&done_bar, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);   // producer's expect_tx arrival (+ TMA bytes)
+      mbar_init(&empty_bar[s], 1);  // tcgen05.commit
     }
+    mbar_init(&done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;");
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -208,68 +173,81 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   const uint32_t tmem = tmem_base;
 
   if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      const int za = a_slots > 1 ? z : 0, zb = b_slots > 1 ? z : 0;
+      for (int kc = 0; kc < nk; ++kc) {
+        const int s = kc % STAGES;
+        if (kc >= STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((kc / STAGES) - 1) & 1));
+        uint8_t* st = smem + s * CF::STAGE;
+        mbar_expect_tx(&full_bar[s], (uint32_t)CF::STAGE);
+        const int k0 = kc * BK;
+#pragma unroll
+        for (int part = 0; part < CF::PARTS; ++part) {
+          uint8_t* sa = st + part * (CF::A_BYTES + CF::B_BYTES);
+          uint8_t* sb = sa + CF::A_BYTES;
+          const CUtensorMap* ma = part ? &maps.a_lo : &maps.a_hi;
+          const CUtensorMap* mb = part ? &maps.b_lo : &maps.b_hi;
+          if (A_MN) {
+#pragma unroll
+            for (int i = 0; i < BM / 32; ++i) tma3(sa + i * 4096, ma, m0 + 32 * i, k0, za, &full_bar[s]);
+          } else {
+            tma3(sa, ma, k0, m0, za, &full_bar[s]);
+          }
+          if (B_MN) {
+#pragma unroll
+            for (int i = 0; i < BN / 32; ++i) tma3(sb + i * 4096, mb, n0 + 32 * i, k0, zb, &full_bar[s]);
+          } else {
+            tma3(sb, mb, k0, n0, zb, &full_bar[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
     // ---------------- MMA issuer
     if (lane == 0) {
-      constexpr uint32_t idesc = make_idesc(BM, BN);
+      constexpr uint32_t idesc = make_idesc(BM, BN, A_MN, B_MN);
+      // K-major: SW128 atoms of 8 rows x 128 B (SBO 1024), K step = 32 B inside the atom.
+      // MN-major (tf32 allows only SW128_32B): atoms of 4 k-rows x 128 B (SBO 512), 32-wide
+      // MN blocks 4 KB apart (LBO), K step = 8 rows = 1024 B.
+      constexpr uint32_t A_STEP = A_MN ? 1024 : 32, B_STEP = B_MN ? 1024 : 32;
+      constexpr uint32_t A_LBO = A_MN ? 4096 : 16, B_LBO = B_MN ? 4096 : 16;
+      constexpr uint32_t A_SBO = A_MN ? 512 : 1024, B_SBO = B_MN ? 512 : 1024;
+      constexpr uint32_t A_LAY = A_MN ? 1 : 2, B_LAY = B_MN ? 1 : 2;
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % STAGES;
         mbar_wait(&full_bar[s], (uint32_t)((kc / STAGES) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;");
-        float* st = smem + s * STAGE;
-        const uint32_t a_hi = smem_u32(st), b_hi = smem_u32(st + A_ELEMS);
-        const uint32_t a_lo = smem_u32(st + A_ELEMS + B_ELEMS);
-        const uint32_t b_lo = a_lo + A_ELEMS * 4;
+        uint8_t* st = smem + s * CF::STAGE;
+        const uint32_t a_hi = smem_u32(st), b_hi = a_hi + CF::A_BYTES;
+        const uint32_t a_lo = b_hi + CF::B_BYTES, b_lo = a_lo + CF::A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < BK / 8; ++ks) {
-          const uint32_t koff = ks * 2 * 128;  // two core matrices along K per MMA
-          const uint64_t ah = make_desc(a_hi + koff), bh = make_desc(b_hi + koff);
+          const uint64_t ah = make_desc(a_hi + ks * A_STEP, A_LBO, A_SBO, A_LAY);
+          const uint64_t bh = make_desc(b_hi + ks * B_STEP, B_LBO, B_SBO, B_LAY);
           mma_tf32(tmem, ah, bh, idesc, (kc > 0 || ks > 0) ? 1u : 0u);
           if (SPLIT) {
-            mma_tf32(tmem, ah, make_desc(b_lo + koff), idesc, 1u);
-            mma_tf32(tmem, make_desc(a_lo + koff), bh, idesc, 1u);
+            mma_tf32(tmem, ah, make_desc(b_lo + ks * B_STEP, B_LBO, B_SBO, B_LAY), idesc, 1u);
+            mma_tf32(tmem, make_desc(a_lo + ks * A_STEP, A_LBO, A_SBO, A_LAY), bh, idesc, 1u);
           }
         }
         mma_commit(&empty_bar[s]);  // stage s may be refilled once these MMAs complete
       }
-      mma_commit(&done_bar);  // accumulator complete
+      mma_commit(&done_bar);  // accumulator complete (arrives at once when nk == 0)
     }
     __syncwarp();
   } else {
-    // ---------------- producers
-    const int p = threadIdx.x - 32;
-    const bool vecA = (A.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(a) & 15) == 0);
-    const bool vecB = (B.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(b) & 15) == 0);
-    using IOA = StageIO<TA, BM>;
-    using IOB = StageIO<!TB, BN>;
-    float4 ra[IOA::Q], rb[IOB::Q];
-    if (nk > 0) {
-      IOA::gload(p, a, A.ld, m0, M, 0, K, vecA, ra);
-      IOB::gload(p, b, B.ld, n0, N, 0, K, vecB, rb);
-    }
-    for (int kc = 0; kc < nk; ++kc) {
-      const int s = kc % STAGES;
-      if (kc >= STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((kc / STAGES) - 1) & 1));
-      float* st = smem + s * STAGE;
-      IOA::sstore(p, ra, st, st + A_ELEMS + B_ELEMS, SPLIT);
-      IOB::sstore(p, rb, st + A_ELEMS, st + A_ELEMS + B_ELEMS + A_ELEMS, SPLIT);
-      if (kc + 1 < nk) {  // next chunk's loads fly while the MMA consumes this stage
-        IOA::gload(p, a, A.ld, m0, M, (kc + 1) * BK, K, vecA, ra);
-        IOB::gload(p, b, B.ld, n0, N, (kc + 1) * BK, K, vecB, rb);
-      }
-      asm volatile("fence.proxy.async.shared::cta;");  // generic smem writes -> async proxy
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&full_bar[s]);
-    }
-    // ---------------- epilogue: TMEM lane group (warp % 4), column half (warp - 1) / 4
+    // ---------------- epilogue: TMEM lane quarter (warp % 4), all BN columns
     mbar_wait(&done_bar, 0u);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int lg = warp & 3;
     const int row = m0 + lg * 32 + lane;
     const uint32_t taddr_row = tmem + ((uint32_t)(lg * 32) << 16);
-    const int half = (warp - 1) >> 2;
-    constexpr int CH = BN / 2;
+    float* __restrict__ c = C.at(z);
+    const bool vecC = (C.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+    const bool empty_k = nk == 0;  // no MMA ran: the product is zero
 #pragma unroll 1
-    for (int cb = half * CH; cb < half * CH + CH; cb += 16) {
+    for (int cb = 0; cb < BN && n0 + cb < N; cb += 16) {
       uint32_t v[16];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
@@ -281,43 +259,178 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
       if (row < M) {
         float* crow = c + (int64_t)row * C.ld;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int col = n0 + cb + j;
-          if (col < N) crow[col] = accumulate ? crow[col] + __uint_as_float(v[j]) : __uint_as_float(v[j]);
+        for (int j4 = 0; j4 < 16; j4 += 4) {
+          const int col = n0 + cb + j4;
+          float o[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o[e] = empty_k ? 0.f : __uint_as_float(v[j4 + e]);
+          if (vecC && col + 3 < N) {
+            float4* p4 = reinterpret_cast<float4*>(crow + col);
+            float4 r4 = make_float4(o[0], o[1], o[2], o[3]);
+            if (accumulate) {
+              const float4 cur = *p4;
+              r4.x += cur.x; r4.y += cur.y; r4.z += cur.z; r4.w += cur.w;
+            }
+            *p4 = r4;
+          } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if (col + e < N) crow[col + e] = accumulate ? crow[col + e] + o[e] : o[e];
+          }
         }
       }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  if (warp == 0)
+  if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
+// ------------------------------------------------------------------ tensor maps (cached)
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+struct MapKey {
+  const void* base;
+  int64_t inner, outer, slots, ld, stride;
+  int64_t box_outer, mn;
+  bool operator==(const MapKey& o) const { return memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    const uint64_t* w = reinterpret_cast<const uint64_t*>(&k);
+    uint64_t h = 1469598103934665603ull;
+    for (size_t i = 0; i < sizeof(MapKey) / 8; ++i) h = (h ^ w[i]) * 1099511628211ull;
+    return (size_t)h;
+  }
+};
+
+std::mutex g_map_mu;
+std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+// 3D fp32 map {inner (contiguous), outer (row stride ld), slots (slot stride)}, box
+// {32, box_outer, 1}, SWIZZLE_128B (K-major) or SWIZZLE_128B_ATOM_32B (MN-major), zero fill
+// out of bounds
+int get_map(const float* base, int64_t inner, int64_t outer, int64_t slots, int64_t ld, int64_t stride,
+            int box_outer, bool mn, CUtensorMap* out) {
+  MapKey key;
+  memset(&key, 0, sizeof(key));
+  key.base = base;
+  key.inner = inner;
+  key.outer = outer;
+  key.slots = slots;
+  key.ld = ld;
+  key.stride = stride;
+  key.box_outer = box_outer;
+  key.mn = mn;
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return SKG_OK;
+    }
+  }
+  auto fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return SKG_ERR_CUDA;
+  }
+  if ((ld * 4) % 16 || (reinterpret_cast<uintptr_t>(base) & 15) || (slots > 1 && (stride * 4) % 16)) {
+    set_error("gemm operand not TMA-compatible (ld / base alignment)");
+    return SKG_ERR_ARG;
+  }
+  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)std::max<int64_t>(slots, 1)};
+  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)std::max<int64_t>(stride, ld * outer) * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)box_outer, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMap m;
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return SKG_ERR_CUDA;
+  }
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = m;
+  *out = m;
+  return SKG_OK;
+}
+
+// operand maps: K-major operands are boxed {32 k, rows}; MN-major {32 mn, 32 k}
+int op_maps(const TcOp& op, bool mn, int64_t mn_extent, int64_t k_extent, int rows_box, int n,
+            bool split, CUtensorMap* hi, CUtensorMap* lo) {
+  const int64_t slots = op.stride ? n : 1;
+  const int64_t inner = mn ? mn_extent : k_extent;
+  const int box_outer = mn ? tc::BK : rows_box;
+  int rc = get_map(op.hi, inner, op.rows_cap, slots, op.ld, op.stride, box_outer, mn, hi);
+  if (rc) return rc;
+  if (split) {
+    if (!op.lo) {
+      set_error("3xTF32 GEMM needs the lo operand");
+      return SKG_ERR_ARG;
+    }
+    rc = get_map(op.lo, inner, op.rows_cap, slots, op.ld, op.stride, box_outer, mn, lo);
+    if (rc) return rc;
+  } else {
+    *lo = *hi;
+  }
+  return SKG_OK;
+}
+
+}  // namespace
+
 template <bool TA, bool TB, int BN, int MODE>
 static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
-                     Act<float> A, Act<float> B, Act<float> C, bool acc, cudaStream_t st) {
-  constexpr int STAGE = (tc::BM * tc::BK + BN * tc::BK) * (MODE == 3 ? 2 : 1);
-  const size_t smem = (size_t)tc::STAGES * STAGE * sizeof(float);
+                     const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st) {
+  using CF = tc::Cfg<BN, MODE>;
+  TcMaps maps;
+  // A: M x K (TA: stored K x M); B: K x N (TB: stored N x K)
+  int rc = op_maps(A, TA, M, K, tc::BM, n, MODE == 3, &maps.a_hi, &maps.a_lo);
+  if (rc) return rc;
+  rc = op_maps(B, !TB, N, K, BN, n, MODE == 3, &maps.b_hi, &maps.b_lo);
+  if (rc) return rc;
   auto kern = k_gemm_tc<TA, TB, BN, MODE>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+    attr = true;
+  }
   dim3 grid((N + BN - 1) / BN, (M + tc::BM - 1) / tc::BM, n);
-  LAUNCH_NAMED("k_gemm_tc", st, kern<<<grid, tc::NTHREADS, smem, st>>>(M, N, K, dM, dK, A, B, C, acc ? 1 : 0));
-  return 0;
+  const int as = A.stride ? n : 1, bs = B.stride ? n : 1;
+  LAUNCH_NAMED("k_gemm_tc", st, kern<<<grid, tc::NTHREADS, CF::SMEM, st>>>(maps, M, N, K, dM, dK, as, bs, C, acc ? 1 : 0));
+  return SKG_OK;
 }
 
 template <bool TA, bool TB, int MODE>
 static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
-                       Act<float> A, Act<float> B, Act<float> C, bool acc, cudaStream_t st) {
-  // narrow N tiles: more CTAs for these skinny problems (M <= a few thousand rows)
+                       const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st) {
+  // 64-wide N tiles: the 3xTF32 issue cost per K step is nearly independent of N up to 256,
+  // and narrow tiles put 4x more CTAs on these skinny problems (M = a few thousand rows)
   if (N <= 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
   return launch_tc<TA, TB, 64, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
 }
 
 int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
-            const int32_t* const* dK, Act<float> A, Act<float> B, Act<float> C, bool acc,
+            const int32_t* const* dK, const TcOp& A, const TcOp& B, Act<float> C, bool acc,
             cudaStream_t st) {
-  if (M <= 0 || N <= 0 || n <= 0) return 0;
+  if (M <= 0 || N <= 0 || n <= 0) return SKG_OK;
 #define TC_CASE(TA_, TB_)                                                                        \
   if (ta == TA_ && tb == TB_)                                                                    \
     return mode == 3 ? dispatch_bn<TA_, TB_, 3>(n, M, N, K, dM, dK, A, B, C, acc, st)            \
@@ -327,7 +440,53 @@ int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_
   TC_CASE(false, true)
   TC_CASE(true, true)
 #undef TC_CASE
-  return 0;
+  return SKG_OK;
+}
+
+// ------------------------------------------------------------------ TF32 splits
+// hi = tf32(x), lo = tf32(x - hi) of a rows x cols matrix (row stride ld_in) into padded
+// outputs (row stride ld_out); padding columns are written as zero
+__global__ void k_split_tf32(const float* __restrict__ in, int64_t ld_in, int64_t rows, int64_t cols,
+                             float* __restrict__ hi, float* __restrict__ lo, int64_t ld_out) {
+  const int64_t total = rows * ld_out;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ld_out, c = i % ld_out;
+    const float x = c < cols ? in[r * ld_in + c] : 0.f;
+    const float h = tf32_rna(x);
+    hi[i] = h;
+    if (lo) lo[i] = tf32_rna(x - h);
+  }
+}
+
+void split_tf32(const float* in, int64_t ld_in, int64_t rows, int64_t cols, float* hi, float* lo,
+                int64_t ld_out, cudaStream_t st) {
+  const int64_t total = rows * ld_out;
+  if (total <= 0) return;
+  const int blocks = (int)std::min<int64_t>((total + 255) / 256, 1184);
+  LAUNCH_NAMED("k_split_tf32", st, (k_split_tf32<<<blocks, 256, 0, st>>>(in, ld_in, rows, cols, hi, lo, ld_out)));
+}
+
+// all layers' weights in one launch: W_l (d_l x d_{l+1}, dense rows) -> padded hi / lo
+__global__ void k_split_weights(WSplitTable t) {
+  for (int l = 0; l < t.L; ++l) {
+    const int64_t rows = t.rows[l], cols = t.cols[l], ldo = t.ld_out[l];
+    const float* in = t.w[l];
+    float* hi = t.hi[l];
+    float* lo = t.lo[l];
+    const int64_t total = rows * ldo;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t r = i / ldo, c = i % ldo;
+      const float x = c < cols ? in[r * cols + c] : 0.f;
+      const float h = tf32_rna(x);
+      hi[i] = h;
+      if (lo) lo[i] = tf32_rna(x - h);
+    }
+  }
+}
+
+void split_weights(const WSplitTable& t, cudaStream_t st) {
+  LAUNCH_NAMED("k_split_weights", st, (k_split_weights<<<296, 256, 0, st>>>(t)));
 }
 
 // test hook: C = op(A) op(B) for host arrays (row-major, ld = inner dim)
@@ -341,14 +500,36 @@ int debug_gemm(int mode, int ta, int tb, int M, int N, int K, const float* hA, c
   cudaMemcpy(dA, hA, na * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(dB, hB, nb * 4, cudaMemcpyHostToDevice);
   cudaMemset(dC, 0, nc * 4);
-  Act<float> a{dA, 0, ta ? M : K}, b{dB, 0, tb ? K : N}, c{dC, 0, N};
-  if (mode == 0) gemm_b<float>(ta, tb, 1, M, N, K, nullptr, nullptr, a, b, c, false, 0);
-  else gemm_tc(mode, ta, tb, 1, M, N, K, nullptr, nullptr, a, b, c, false, 0);
+  int rc = SKG_OK;
+  if (mode == 0) {
+    Act<float> a{dA, 0, ta ? M : K}, b{dB, 0, tb ? K : N}, c{dC, 0, N};
+    gemm_simt<float>(ta, tb, 1, M, N, K, nullptr, nullptr, a, b, c, false, 0);
+  } else {
+    // stored shapes: A (TA ? K x M : M x K), B (TB ? N x K : K x N); split into padded buffers
+    const int64_t ar = ta ? K : M, ac = ta ? M : K, br = tb ? N : K, bc = tb ? K : N;
+    const int64_t lda = round4(ac), ldb = round4(bc);
+    float *ah, *al, *bh, *bl;
+    cudaMalloc(&ah, std::max<int64_t>(ar * lda, 1) * 4);
+    cudaMalloc(&al, std::max<int64_t>(ar * lda, 1) * 4);
+    cudaMalloc(&bh, std::max<int64_t>(br * ldb, 1) * 4);
+    cudaMalloc(&bl, std::max<int64_t>(br * ldb, 1) * 4);
+    split_tf32(dA, ac, ar, ac, ah, mode == 3 ? al : nullptr, lda, 0);
+    split_tf32(dB, bc, br, bc, bh, mode == 3 ? bl : nullptr, ldb, 0);
+    TcOp A{ah, mode == 3 ? al : nullptr, lda, 0, ar}, B{bh, mode == 3 ? bl : nullptr, ldb, 0, br};
+    Act<float> c{dC, 0, N};
+    rc = gemm_tc(mode, ta, tb, 1, M, N, K, nullptr, nullptr, A, B, c, false, 0);
+    cudaDeviceSynchronize();
+    cudaFree(ah);
+    cudaFree(al);
+    cudaFree(bh);
+    cudaFree(bl);
+  }
   cudaError_t e = cudaDeviceSynchronize();
   cudaMemcpy(hC, dC, nc * 4, cudaMemcpyDeviceToHost);
   cudaFree(dA);
   cudaFree(dB);
   cudaFree(dC);
+  if (rc) return rc;
   if (e != cudaSuccess) {
     set_error(std::string("debug_gemm: ") + cudaGetErrorString(e));
     return SKG_ERR_CUDA;
@@ -361,4 +542,43 @@ int debug_gemm(int mode, int ta, int tb, int M, int N, int K, const float* hA, c
 extern "C" int skg_debug_gemm(int mode, int ta, int tb, int M, int N, int K, const float* A,
                               const float* B, float* C) {
   return skg::debug_gemm(mode, ta, tb, M, N, K, A, B, C);
+}
+
+// debug: time `iters` GEMMs on device-resident (zero) split operands, M x K by K x N
+extern "C" int skg_debug_gemm_timed(int mode, int ta, int tb, int M, int N, int K, int iters,
+                                    float* us_out) {
+  using namespace skg;
+  const int64_t ar = ta ? K : M, ac = ta ? M : K, br = tb ? N : K, bc = tb ? K : N;
+  const int64_t lda = round4(ac), ldb = round4(bc);
+  float *ah, *al, *bh, *bl, *dC;
+  cudaMalloc(&ah, ar * lda * 4);
+  cudaMalloc(&al, ar * lda * 4);
+  cudaMalloc(&bh, br * ldb * 4);
+  cudaMalloc(&bl, br * ldb * 4);
+  cudaMalloc(&dC, (size_t)M * N * 4);
+  cudaMemset(ah, 0, ar * lda * 4);
+  cudaMemset(al, 0, ar * lda * 4);
+  cudaMemset(bh, 0, br * ldb * 4);
+  cudaMemset(bl, 0, br * ldb * 4);
+  TcOp A{ah, al, lda, 0, ar}, B{bh, bl, ldb, 0, br};
+  Act<float> c{dC, 0, N};
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int rc = 0;
+  for (int i = 0; i < 3; ++i) rc |= gemm_tc(mode, ta, tb, 1, M, N, K, nullptr, nullptr, A, B, c, false, 0);
+  cudaEventRecord(e0, 0);
+  for (int i = 0; i < iters; ++i) gemm_tc(mode, ta, tb, 1, M, N, K, nullptr, nullptr, A, B, c, false, 0);
+  cudaEventRecord(e1, 0);
+  cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  *us_out = ms * 1000.f / iters;
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaFree(ah);
+  cudaFree(al);
+  cudaFree(bh);
+  cudaFree(bl);
+  cudaFree(dC);
+  return (rc || e != cudaSuccess) ? -1 : 0;
 }

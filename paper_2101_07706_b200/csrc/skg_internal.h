@@ -28,6 +28,8 @@ std::string repr_int(int64_t v);
 void set_error(const std::string& msg);
 const char* last_error();
 
+static inline int64_t round4(int64_t d) { return (d + 3) / 4 * 4; }
+
 // Status codes are the SKG_* macros of include/skewgcn_b200.h.
 
 // Device error-flag bits written by kernels into PlanDev::err
