@@ -184,20 +184,25 @@ def run_ours(args):
     d_ids = torch.as_tensor(ids, device="cuda")
     workers = np.array(tr.mine * T, dtype=np.int32)
 
-    def sample_resident(s0, n):
-        check(lib.skg_ladies_sample_device(
-            tr.ps.h, n * n_my, ptr(workers, C.c_int32),
-            ptr(np.ascontiguousarray(bl[s0:s0 + n].reshape(-1)), C.c_int32),
-            d_ids[s0].data_ptr(), args.batch, MODES[args.mode], float(args.D), 1.0,
-            ptr(np.ascontiguousarray(states[s0:s0 + n].reshape(-1, 4)), C.c_uint64), tr.stream))
+    def sample_resident(s0, n, buf):
+        tr.sample_device(buf, n * n_my, workers, np.ascontiguousarray(bl[s0:s0 + n].reshape(-1)),
+                         d_ids[s0].data_ptr(), args.batch,
+                         np.ascontiguousarray(states[s0:s0 + n].reshape(-1, 4)))
 
     def steps_resident(s0, count):
-        for g0 in range(s0, s0 + count, T):
-            n = min(T, s0 + count - g0)
-            sample_resident(g0, n)
-            for gi in range(n):
-                tr.compute(0, (g0 + gi) % per, gi)
+        # the Trainer's pipeline: group g+1 sampled on the side stream while the GCN of
+        # group g runs on the main stream (double-buffered plan arenas)
+        groups = [(g0, min(T, s0 + count - g0)) for g0 in range(s0, s0 + count, T)]
+        sample_resident(groups[0][0], groups[0][1], 0)
+        for gi, (g0, n) in enumerate(groups):
+            b = gi % 2
+            if gi + 1 < len(groups):
+                sample_resident(groups[gi + 1][0], groups[gi + 1][1], 1 - b)
+            tr.wait_sampled(b)
+            for i in range(n):
+                tr.compute(0, (g0 + i) % per, i, b)
                 tr.reduce_and_step()
+            tr.release_buf(b)
 
     def barrier():
         if dist is not None:
@@ -211,6 +216,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
+        tr.side.wait_event(ev0)  # the side (sampler) stream starts inside the timed region
         steps_resident(W, K)
         ev1.record(stream)
         barrier()
@@ -228,24 +234,31 @@ def run_ours(args):
     if dist is not None:
         dist.all_reduce(ledger)
     remote_per_iter = float(ledger.sum().item()) / (W + K)
-    stats = [tr.ps.stats(i)[0] for i in range(n_my * T)]
+    torch.cuda.synchronize()
+    stats = [tr.bufs[0][0].stats(i)[0] for i in range(n_my * T)]
     s0_remote = sum(int(st[N_LAYERS - 1, 4]) for st in stats) / T   # input-layer rows moved
     sampled_nodes = sum(int(st[:, 2].sum()) for st in stats) / T
     alg_bytes = sum(algorithmic_sampler_bytes(st) for st in stats)   # one T-plan launch
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     samp_ms, comp_ms = [], []
-    for rep in range(3):
+    for rep in range(3):  # stages run back to back here (no overlap) to time each alone
         s0 = W + (rep * T) % K
-        ev[0].record(stream)
-        sample_resident(s0, T)
-        ev[1].record(stream)
-        for gi in range(T):
-            tr.compute(0, (s0 + gi) % per, gi)
-            tr.reduce_and_step()
+        torch.cuda.synchronize()
+        ev[0].record(tr.side)
+        sample_resident(s0, T, 0)
+        ev[1].record(tr.side)
+        tr.wait_sampled(0)
+        torch.cuda.synchronize()
         ev[2].record(stream)
+        ev[3].record(stream)
+        for gi in range(T):
+            tr.compute(0, (s0 + gi) % per, gi, 0)
+            tr.reduce_and_step()
+        ev[4].record(stream)
+        tr.release_buf(0)
         torch.cuda.synchronize()
         samp_ms.append(ev[0].elapsed_time(ev[1]))
-        comp_ms.append(ev[1].elapsed_time(ev[2]) / T)
+        comp_ms.append(ev[3].elapsed_time(ev[4]) / T)
     samp = float(np.median(samp_ms))
     peaks = {}
     try:
@@ -264,14 +277,31 @@ def run_ours(args):
     barrier()
     h2d = [0]
 
+    # each step's loss is copied to pinned host memory behind its GCN on the main stream and
+    # read by the host two steps later (no per-step stream drain); all are read in the region
+    ring = [torch.empty(n_my, dtype=torch.float64, pin_memory=True) for _ in range(4)]
+    ring_ev = [torch.cuda.Event() for _ in range(4)]
+    pending, host_losses = [], []
+
     def read_loss(e, it):
         h2d[0] += int(tr._boff[n_my]) * 4 + n_my * 32
-        _ = tr.losses[it % per].cpu()  # the step's result to host
+        i = len(host_losses) + len(pending)
+        ring[i % 4].copy_(tr.losses[it % per], non_blocking=True)
+        ring_ev[i % 4].record(stream)
+        pending.append(i)
+        while len(pending) > 2:
+            j = pending.pop(0)
+            ring_ev[j % 4].synchronize()
+            host_losses.append(float(ring[j % 4].sum()))
 
     pairs = [(s // per, s % per) for s in range(K)]
     t_e2e0 = time.perf_counter()
     tr.run(pairs, on_iteration=read_loss)
+    for j in pending:
+        ring_ev[j % 4].synchronize()
+        host_losses.append(float(ring[j % 4].sum()))
     barrier()
+    assert len(host_losses) == K and all(np.isfinite(host_losses)), "e2e: step losses not all read
     e2e_ms = (time.perf_counter() - t_e2e0) * 1e3
     if dist is not None:
         t = torch.tensor([e2e_ms], device="cuda")

@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cstddef>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -337,6 +338,7 @@ extern "C" int skg_ctx_create(int device, int64_t n, int64_t nnz, const int64_t*
   }
   CK(cudaMemcpy(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost));
   c->normalized = (n > 0) && !bad;
+  if (getenv("SKG_STORED_WEIGHTS")) c->normalized = false;  // experiment: read w, never recompute
   cudaFree(d_bad);
   if (!c->symmetric) {  // host counting sort by column (rows ascending within a column)
     std::vector<int64_t> toff(n + 1, 0);

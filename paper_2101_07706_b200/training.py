@@ -516,12 +516,17 @@ class Trainer:
         self.dg.ensure_features(g.features, self.dtype)
         self.dg.ensure_labels(np.asarray(g.labels))
         n_slots = max(1, self.n_my * self.ahead)
-        if sampler == "ladies":
-            self.ps = self.dg.acquire(KIND_LADIES, n_slots, self.L, int(self.cfg.budget), int(batch_size))
-        else:
-            self.ps = self.dg.acquire(KIND_SAINT, n_slots, self.L, int(subgraph_size), 1)
-            _saint_set(self.dg, self.ps, self.all_train, mode != "local")
-        self.gcn = self.ps.gcn(self.dims, self.dtype)
+        # two plan arenas: the sampler fills one (side stream) while the GCN consumes the
+        # other (main stream); plans never depend on the weights (training.py:488-493)
+        self.bufs = []
+        for _ in range(2):
+            if sampler == "ladies":
+                ps = self.dg.acquire(KIND_LADIES, n_slots, self.L, int(self.cfg.budget), int(batch_size))
+            else:
+                ps = self.dg.acquire(KIND_SAINT, n_slots, self.L, int(subgraph_size), 1)
+                _saint_set(self.dg, ps, self.all_train, mode != "local")
+            self.bufs.append((ps, ps.gcn(self.dims, self.dtype)))
+        self.ps, self.gcn = self.bufs[0]
         self._peer_ptrs = []
         if shard_features is None:
             shard_features = self.world > 1
@@ -550,6 +555,13 @@ class Trainer:
         self.losses = torch.zeros((self.per_epoch, max(1, self.n_my)), dtype=torch.float64,
                                   device="cuda")
         self.stream = D.current_stream()
+        self.main = torch.cuda.current_stream()
+        # high priority: the sampler is the longer stage; GCN kernels fill its idle SMs
+        self.side = torch.cuda.Stream(priority=-1)
+        self.side_h = C.c_void_p(self.side.cuda_stream)
+        self.ev_sampled = [torch.cuda.Event(), torch.cuda.Event()]
+        self.ev_used = [torch.cuda.Event(), torch.cuda.Event()]
+        self._used_armed = [False, False]
         self.dtc = DT[self.dtype]
         self._workers = np.array(self.mine * self.ahead, dtype=np.int32)
         self._states = np.zeros((n_slots, 4), dtype=np.uint64)
@@ -604,39 +616,71 @@ class Trainer:
                 self._states[s] = pcg64_state(self.seed, "plan", epoch, it, w)
         return self._boff, self._bids, self._states
 
-    def sample_group(self, pairs):
-        """Sample the plans of iterations ``pairs`` = [(epoch, it), ...] in one launch."""
+    def sample_group(self, pairs, buf=0):
+        """Sample the plans of iterations ``pairs`` = [(epoch, it), ...] in one launch
+        sequence into plan arena ``buf``, on the side stream."""
         assert 1 <= len(pairs) <= self.ahead
         self._boff[0] = 0
         for gi, (e, it) in enumerate(pairs):
             self.host_inputs(e, it, gi)
         self._group = list(pairs)
-        self.sample(len(pairs) * self.n_my)
+        self.sample(len(pairs) * self.n_my, buf)
 
-    def sample(self, n=None):
+    def _begin_sample(self, buf):
+        # the arena may still be read by the GCN of the group that used it last
+        if self._used_armed[buf]:
+            self.side.wait_event(self.ev_used[buf])
+
+    def _end_sample(self, buf):
+        self.ev_sampled[buf].record(self.side)
+
+    def sample(self, n=None, buf=0):
         n = self.n_my if n is None else n
         if n == 0:
             return
+        ps = self.bufs[buf][0]
+        self._begin_sample(buf)
         if self.sampler == "ladies":
-            check(lib.skg_ladies_sample(self.ps.h, n, ptr(self._workers, C.c_int32),
+            check(lib.skg_ladies_sample(ps.h, n, ptr(self._workers, C.c_int32),
                                         ptr(self._boff, C.c_int64), ptr(self._bids, C.c_int64),
                                         MODES[self.mode], float(self.cfg.skew_constant),
                                         float(self.cfg.min_scale), ptr(self._states, C.c_uint64),
-                                        self.stream))
+                                        self.side_h))
         else:
-            check(lib.skg_saint_sample(self.ps.h, n, ptr(self._workers, C.c_int32), MODES[self.mode],
+            check(lib.skg_saint_sample(ps.h, n, ptr(self._workers, C.c_int32), MODES[self.mode],
                                        float(self.cfg.skew_constant), float(self.cfg.min_scale),
-                                       ptr(self._states, C.c_uint64), self.stream))
+                                       ptr(self._states, C.c_uint64), self.side_h))
+        self._end_sample(buf)
+
+    def sample_device(self, buf, n, workers, batch_len, d_batch, batch_stride, states):
+        """LADIES sampling from device-resident batch ids (benchmark inputs)."""
+        ps = self.bufs[buf][0]
+        self._begin_sample(buf)
+        check(lib.skg_ladies_sample_device(
+            ps.h, n, ptr(workers, C.c_int32), ptr(batch_len, C.c_int32), d_batch, batch_stride,
+            MODES[self.mode], float(self.cfg.skew_constant), float(self.cfg.min_scale),
+            ptr(states, C.c_uint64), self.side_h))
+        self._end_sample(buf)
+
+    def wait_sampled(self, buf):
+        """Order the main stream after the sampling of arena ``buf``."""
+        self.main.wait_event(self.ev_sampled[buf])
+
+    def release_buf(self, buf):
+        """Mark arena ``buf`` free for the next sampling once the queued GCN work ends."""
+        self.ev_used[buf].record(self.main)
+        self._used_armed[buf] = True
 
     # -- compute (training.py:499-506) --------------------------------------
-    def compute(self, epoch, it, group=0):
+    def compute(self, epoch, it, group=0, buf=0):
         if self.n_my:
+            ps, gcn = self.bufs[buf]
             s0 = group * self.n_my
             # all of this rank's workers in one batched pass; gradients summed in worker order
-            check(lib.skg_gcn_step_batch(self.gcn, s0, self.n_my, ptr(self.wp, C.c_uint64),
+            check(lib.skg_gcn_step_batch(gcn, s0, self.n_my, ptr(self.wp, C.c_uint64),
                                          ptr(self.gp, C.c_uint64), 0,
                                          self.losses[it % self.per_epoch].data_ptr(), self.stream))
-            check(lib.skg_plans_ledger_add(self.ps.h, s0, self.n_my,
+            check(lib.skg_plans_ledger_add(ps.h, s0, self.n_my,
                                            self.ledger[epoch % self.ledger.shape[0]].data_ptr(),
                                            self.stream))
         else:
@@ -656,25 +700,39 @@ class Trainer:
                                     float(self.lr), contrib, self.t, self.stream))
 
     def iteration(self, epoch, it):
-        self.sample_group([(epoch, it)])
-        self.compute(epoch, it)
+        self.sample_group([(epoch, it)], 0)
+        self.wait_sampled(0)
+        self.compute(epoch, it, 0, 0)
         self.reduce_and_step()
+        self.release_buf(0)
 
     def run(self, pairs, on_iteration=None):
-        """Train over iterations ``pairs`` in order, sampling ``ahead`` iterations at once."""
-        for g0 in range(0, len(pairs), self.ahead):
-            chunk = pairs[g0:g0 + self.ahead]
-            self.sample_group(chunk)
-            for gi, (e, it) in enumerate(chunk):
-                self.compute(e, it, gi)
+        """Train over iterations ``pairs`` in order, ``ahead`` iterations of plans per
+        sampling launch; group g+1 is sampled on the side stream while the GCN of group g
+        runs on the main stream (double-buffered plan arenas)."""
+        groups = [pairs[g0:g0 + self.ahead] for g0 in range(0, len(pairs), self.ahead)]
+        if not groups:
+            return
+        self.sample_group(groups[0], 0)
+        for gi, chunk in enumerate(groups):
+            b = gi % 2
+            if gi + 1 < len(groups):
+                self.sample_group(groups[gi + 1], 1 - b)
+            self.wait_sampled(b)
+            for ci, (e, it) in enumerate(chunk):
+                self.compute(e, it, ci, b)
                 self.reduce_and_step()
                 if on_iteration is not None:
                     on_iteration(e, it)
+            self.release_buf(b)
 
     def check_errors(self):
-        for i in range(self.ps.n_slots):
-            _, info, rc = self.ps.stats(i)
-            check(rc)
+        torch = _torch()
+        torch.cuda.synchronize()
+        for ps, _ in self.bufs:
+            for i in range(ps.n_slots):
+                _, info, rc = ps.stats(i)
+                check(rc)
 
     def weights_to_model(self):
         for w, v in zip(self.model.weights, self.wviews):
@@ -688,7 +746,9 @@ class Trainer:
             X = self.g.features
             self.dg.feat_key = None
             self.dg.ensure_features(X, self.dtype)
-        self.dg.release(self.ps)
+        _torch().cuda.synchronize()
+        for ps, _ in self.bufs:
+            self.dg.release(ps)
 
 
 def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, cfg: SamplerConfig, *,
