@@ -301,7 +301,7 @@ def run_ours(args):
         ring_ev[j % 4].synchronize()
         host_losses.append(float(ring[j % 4].sum()))
     barrier()
-    assert len(host_losses) == K and all(np.isfinite(host_losses)), "e2e: step losses not all read
+    assert len(host_losses) == K and all(np.isfinite(host_losses)), "e2e: step losses not all read"
     e2e_ms = (time.perf_counter() - t_e2e0) * 1e3
     if dist is not None:
         t = torch.tensor([e2e_ms], device="cuda")

@@ -552,6 +552,8 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     cap_batch = 1;
   }
   ARG(cap_pairs < (1LL << 31) && cap_cand < (1LL << 31), "plan capacity exceeds int32 indexing");
+  // LADIES keeps upper-row ranks in 16-bit slots / counters
+  ARG(kind != KIND_LADIES || cap_rows < 65535, "LADIES batch / budget must be below 65535");
   ps->cap_rows = (int)cap_rows;
   ps->cap_cand = (int)cap_cand;
   ps->cap_pairs = cap_pairs;
@@ -590,16 +592,23 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     cv.add(P.bitmap, n_words);
     cv.add(P.sbitmap, n_words);
     cv.add(P.cnt_pack, (size_t)(n / 2 + 1));
-    cv.add(P.fill, kind == KIND_LADIES ? cap_cand : 1);
+    const bool lad = kind == KIND_LADIES, stw = lad && !c->normalized;
+    cv.add(P.slots, lad ? (size_t)std::max<int64_t>(n, 1) * kSlots : 4);
+    cv.add(P.slotw, stw ? (size_t)std::max<int64_t>(n, 1) * kSlots : 1);
+    cv.add(P.ov, lad ? cap_pairs : 1);
+    cv.add(P.ovw, stw ? cap_pairs : 1);
+    cv.add(P.hidx, lad ? (size_t)std::max<int64_t>(n, 1) : 1);
+    cv.add(P.hoff, lad ? cap_cand : 1);
+    cv.add(P.hfill, lad ? cap_cand : 1);
+    cv.add(P.hbuf, lad ? cap_pairs : 1);
+    cv.add(P.hbufw, stw ? cap_pairs : 1);
+    cv.add(P.heavy, lad ? cap_cand : 1);
+    cv.add(P.huge, lad ? cap_cand : 1);
+    cv.add(P.updeg, lad ? cap_rows : 1);
+    cv.add(P.cand_cnt, lad ? cap_cand : 1);
     cv.add(P.pair_off, cap_rows + 1);
     cv.add(P.word_prefix, n_words);
     cv.add(P.tile_a, cap_tiles);
-    cv.add(P.tile_b, cap_tiles);
-    cv.add(P.tile_c, cap_tiles);
-    cv.add(P.bucket_off, kind == KIND_LADIES ? cap_cand + 1 : 1);
-    cv.add(P.bucket_r, kind == KIND_LADIES ? cap_pairs : 1);
-    cv.add(P.bucket_w, (kind == KIND_LADIES && !c->normalized) ? cap_pairs : 1);
-    cv.add(P.big_list, kind == KIND_LADIES ? cap_cand : 1);
     cv.add(P.pw_val, cap_slots);
     cv.add(P.pw_lvl, cap_slots);
     cv.add(P.chunk_sum, cap_chunks);

@@ -66,17 +66,26 @@ struct PlanDev {
   uint32_t* bitmap;         // [n_words]
   uint32_t* sbitmap;        // [n_words] sampled set
   uint32_t* cnt_pack;       // [n/2+1] 16-bit pair counters per node, zero at rest
-  int32_t* fill;            // [cap_cand] bucket fill counters
+  // LADIES contributions (upper-row rank r of every pair (r, j)), by node: the first
+  // kSlots arrivals in slots[j], later ones in the overflow list; candidates with more
+  // than kSlots get a contiguous, row-sorted range hbuf[hoff[h] .. + count)
+  uint16_t* slots;          // [n*kSlots]
+  double* slotw;            // [n*kSlots] stored w_ij (graphs that are not normalised)
+  int2* ov;                 // [cap_pairs] overflow pairs (j, r)
+  double* ovw;              // [cap_pairs] (not normalised)
+  int32_t* hidx;            // [n] node -> heavy index
+  int32_t* hoff;            // [cap_cand] heavy range starts
+  int32_t* hfill;           // [cap_cand] heavy fill counters
+  int32_t* hbuf;            // [cap_pairs] heavy entries (row-sorted after the heavy fold)
+  double* hbufw;            // [cap_pairs] (not normalised)
+  int32_t* heavy;           // [cap_cand] candidate ranks with count > kSlots
+  int32_t* huge;            // [cap_cand] heavy candidates with count > 32
+  double* updeg;            // [cap_rows] degree of each upper row (normalised graphs)
+  int32_t* cand_cnt;        // [cap_cand] contributions per candidate
   int64_t* pair_off;        // [cap_rows+1]
   int32_t* word_prefix;     // [n_words]
   int64_t* tile_a;          // [cap_tiles]
-  int64_t* tile_b;          // [cap_tiles]
-  int64_t* tile_c;          // [cap_tiles]
-  int32_t* bucket_off;      // [cap_cand+1]
-  int32_t* bucket_r;        // [cap_pairs]
-  double* bucket_w;         // [cap_pairs] (only for graphs that are not normalised)
-  int32_t* big_list;        // [cap_cand]
-  int32_t* counters;        // [8]: 0 big_count
+  int32_t* counters;        // [8]: 0 heavy, 1 overflow, 2 huge
   double* pw_val;           // [cap_slots]
   int32_t* pw_lvl;          // [cap_slots]
   double* chunk_sum;        // [cap_chunks]
@@ -110,6 +119,7 @@ struct PlanDev {
   LayerStat* stat;          // [L]
 };
 
+constexpr int kSlots = 4;         // contributions kept per node before overflowing
 constexpr int kTileWords = 256;    // bitmap words per compaction tile (8 warps x 32 words)
 constexpr int kTileCand = 4096;    // candidates per scan tile
 constexpr int kSmallBucket = 16;   // buckets folded in registers

@@ -40,3 +40,12 @@ def test_library_is_sm100a():
     if out.returncode != 0:
         pytest.skip("cuobjdump unavailable")
     assert "sm_100a" in out.stdout
+
+
+def test_scripts_parse():
+    """bench.py and the driver entry point must at least parse (the driver runs them)."""
+    import ast
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    for f in ("bench.py", "__graft_entry__.py"):
+        ast.parse((root / f).read_text())
