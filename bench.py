@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ahead", type=int, default=4, help="iterations of plans per sampler launch")
+    ap.add_argument("--streams", type=int, default=2, help="sampler streams (groups in flight)")
     return ap.parse_args()
 
 
@@ -161,7 +162,7 @@ def run_ours(args):
     P.set_compute_dtype(args.dtype)
     T = max(1, args.ahead)
     tr = P.Trainer(g, part, model, cfg, batch_size=args.batch, lr=args.lr, mode=args.mode,
-                   seed=0, dtype=args.dtype, epochs=1, ahead=T)
+                   seed=0, dtype=args.dtype, epochs=1, ahead=T, streams=args.streams)
     stream = torch.cuda.current_stream()
     n_my = tr.n_my
     W = max(args.warmup, 1)
@@ -190,19 +191,17 @@ def run_ours(args):
                          np.ascontiguousarray(states[s0:s0 + n].reshape(-1, 4)))
 
     def steps_resident(s0, count):
-        # the Trainer's pipeline: group g+1 sampled on the side stream while the GCN of
-        # group g runs on the main stream (double-buffered plan arenas)
+        # the Trainer's pipeline: groups sampled ahead on the sampler streams into rotating
+        # plan arenas while the GCN consumes them in order on the main stream
         groups = [(g0, min(T, s0 + count - g0)) for g0 in range(s0, s0 + count, T)]
-        sample_resident(groups[0][0], groups[0][1], 0)
-        for gi, (g0, n) in enumerate(groups):
-            b = gi % 2
-            if gi + 1 < len(groups):
-                sample_resident(groups[gi + 1][0], groups[gi + 1][1], 1 - b)
-            tr.wait_sampled(b)
+
+        def compute(g, b):
+            g0, n = groups[g]
             for i in range(n):
                 tr.compute(0, (g0 + i) % per, i, b)
                 tr.reduce_and_step()
-            tr.release_buf(b)
+
+        tr.pipeline(len(groups), lambda g, b: sample_resident(groups[g][0], groups[g][1], b), compute)
 
     def barrier():
         if dist is not None:
@@ -216,7 +215,8 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
-        tr.side.wait_event(ev0)  # the side (sampler) stream starts inside the timed region
+        for sd in tr.sides:  # the sampler streams start inside the timed region
+            sd.wait_event(ev0)
         steps_resident(W, K)
         ev1.record(stream)
         barrier()
@@ -331,6 +331,7 @@ def run_ours(args):
                                    f"{N_LAYERS} layers hidden {DIMS_HIDDEN}",
                        "n_nodes": sg.n_nodes, "nnz": sg.nnz, "workers": k,
                        "plans_per_sampler_launch": T * n_my, "lookahead_iters": T,
+                       "sampler_streams": args.streams,
                        "l2": "inputs > L2 (114M-entry CSR, 561 MB features); no flush"},
             "remote_nodes_per_iter": round(remote_per_iter, 2),
             "input_layer_remote_rows_per_iter": s0_remote,

@@ -470,7 +470,7 @@ class Trainer:
 
     def __init__(self, g, partition, model, cfg, *, batch_size, lr, mode, seed,
                  sampler="ladies", subgraph_size=None, optimizer="sgd", dtype=None,
-                 epochs=1, workers=None, ahead=1, shard_features=None):
+                 epochs=1, workers=None, ahead=1, shard_features=None, streams=1):
         torch = _torch()
         if g.features is None or g.labels is None or g.train_mask is None:
             raise ValueError("training needs features, labels and masks")
@@ -516,10 +516,13 @@ class Trainer:
         self.dg.ensure_features(g.features, self.dtype)
         self.dg.ensure_labels(np.asarray(g.labels))
         n_slots = max(1, self.n_my * self.ahead)
-        # two plan arenas: the sampler fills one (side stream) while the GCN consumes the
-        # other (main stream); plans never depend on the weights (training.py:488-493)
+        # plan arenas in rotation: `streams` sampler streams fill groups ahead while the GCN
+        # consumes the oldest one (main stream); plans never depend on the weights
+        # (training.py:488-493)
+        self.n_streams = max(1, int(streams))
+        self.n_bufs = self.n_streams + 1
         self.bufs = []
-        for _ in range(2):
+        for _ in range(self.n_bufs):
             if sampler == "ladies":
                 ps = self.dg.acquire(KIND_LADIES, n_slots, self.L, int(self.cfg.budget), int(batch_size))
             else:
@@ -557,11 +560,12 @@ class Trainer:
         self.stream = D.current_stream()
         self.main = torch.cuda.current_stream()
         # high priority: the sampler is the longer stage; GCN kernels fill its idle SMs
-        self.side = torch.cuda.Stream(priority=-1)
-        self.side_h = C.c_void_p(self.side.cuda_stream)
-        self.ev_sampled = [torch.cuda.Event(), torch.cuda.Event()]
-        self.ev_used = [torch.cuda.Event(), torch.cuda.Event()]
-        self._used_armed = [False, False]
+        self.sides = [torch.cuda.Stream(priority=-1) for _ in range(self.n_streams)]
+        self.side = self.sides[0]
+        self.ev_sampled = [torch.cuda.Event() for _ in range(self.n_bufs)]
+        self.ev_used = [torch.cuda.Event() for _ in range(self.n_bufs)]
+        self._used_armed = [False] * self.n_bufs
+        self._buf_stream = [self.sides[b % self.n_streams] for b in range(self.n_bufs)]
         self.dtc = DT[self.dtype]
         self._workers = np.array(self.mine * self.ahead, dtype=np.int32)
         self._states = np.zeros((n_slots, 4), dtype=np.uint64)
@@ -626,13 +630,16 @@ class Trainer:
         self._group = list(pairs)
         self.sample(len(pairs) * self.n_my, buf)
 
+    def _stream_of(self, buf):
+        return self._buf_stream[buf]
+
     def _begin_sample(self, buf):
         # the arena may still be read by the GCN of the group that used it last
         if self._used_armed[buf]:
-            self.side.wait_event(self.ev_used[buf])
+            self._stream_of(buf).wait_event(self.ev_used[buf])
 
     def _end_sample(self, buf):
-        self.ev_sampled[buf].record(self.side)
+        self.ev_sampled[buf].record(self._stream_of(buf))
 
     def sample(self, n=None, buf=0):
         n = self.n_my if n is None else n
@@ -645,11 +652,12 @@ class Trainer:
                                         ptr(self._boff, C.c_int64), ptr(self._bids, C.c_int64),
                                         MODES[self.mode], float(self.cfg.skew_constant),
                                         float(self.cfg.min_scale), ptr(self._states, C.c_uint64),
-                                        self.side_h))
+                                        C.c_void_p(self._stream_of(buf).cuda_stream)))
         else:
             check(lib.skg_saint_sample(ps.h, n, ptr(self._workers, C.c_int32), MODES[self.mode],
                                        float(self.cfg.skew_constant), float(self.cfg.min_scale),
-                                       ptr(self._states, C.c_uint64), self.side_h))
+                                       ptr(self._states, C.c_uint64),
+                                       C.c_void_p(self._stream_of(buf).cuda_stream)))
         self._end_sample(buf)
 
     def sample_device(self, buf, n, workers, batch_len, d_batch, batch_stride, states):
@@ -659,7 +667,7 @@ class Trainer:
         check(lib.skg_ladies_sample_device(
             ps.h, n, ptr(workers, C.c_int32), ptr(batch_len, C.c_int32), d_batch, batch_stride,
             MODES[self.mode], float(self.cfg.skew_constant), float(self.cfg.min_scale),
-            ptr(states, C.c_uint64), self.side_h))
+            ptr(states, C.c_uint64), C.c_void_p(self._stream_of(buf).cuda_stream)))
         self._end_sample(buf)
 
     def wait_sampled(self, buf):
@@ -706,25 +714,36 @@ class Trainer:
         self.reduce_and_step()
         self.release_buf(0)
 
+    def pipeline(self, n_groups, sample_fn, compute_fn):
+        """Drive groups 0..n_groups-1: group g is sampled into arena g % n_bufs on sampler
+        stream g % n_streams up to n_streams groups ahead of the GCN, which consumes the
+        groups in order on the main stream (``sample_fn(g, buf)``, ``compute_fn(g, buf)``)."""
+        if n_groups <= 0:
+            return
+        S, NB = self.n_streams, self.n_bufs
+        for g in range(min(S, n_groups)):
+            sample_fn(g, g % NB)
+        for g in range(n_groups):
+            b = g % NB
+            self.wait_sampled(b)
+            compute_fn(g, b)
+            self.release_buf(b)
+            if g + S < n_groups:  # its arena was used by group g - 1, released above
+                sample_fn(g + S, (g + S) % NB)
+
     def run(self, pairs, on_iteration=None):
         """Train over iterations ``pairs`` in order, ``ahead`` iterations of plans per
-        sampling launch; group g+1 is sampled on the side stream while the GCN of group g
-        runs on the main stream (double-buffered plan arenas)."""
+        sampling launch, sampled ahead of the GCN on the sampler streams."""
         groups = [pairs[g0:g0 + self.ahead] for g0 in range(0, len(pairs), self.ahead)]
-        if not groups:
-            return
-        self.sample_group(groups[0], 0)
-        for gi, chunk in enumerate(groups):
-            b = gi % 2
-            if gi + 1 < len(groups):
-                self.sample_group(groups[gi + 1], 1 - b)
-            self.wait_sampled(b)
-            for ci, (e, it) in enumerate(chunk):
+
+        def compute(g, b):
+            for ci, (e, it) in enumerate(groups[g]):
                 self.compute(e, it, ci, b)
                 self.reduce_and_step()
                 if on_iteration is not None:
                     on_iteration(e, it)
-            self.release_buf(b)
+
+        self.pipeline(len(groups), lambda g, b: self.sample_group(groups[g], b), compute)
 
     def check_errors(self):
         torch = _torch()
@@ -754,7 +773,7 @@ class Trainer:
 def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, cfg: SamplerConfig, *,
                       epochs: int, batch_size: int, lr: float, mode: str, seed: int,
                       sampler: str = "ladies", subgraph_size: int | None = None,
-                      optimizer: str = "sgd", ahead: int = 4) -> tuple:
+                      optimizer: str = "sgd", ahead: int = 4, streams: int = 2) -> tuple:
     """Data-parallel training with per-iteration gradient averaging (training.py:430-518).
 
     Single process: all workers run on this GPU.  Under torch.distributed (one process
@@ -765,7 +784,7 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
     torch = _torch()
     tr = Trainer(g, partition, model, cfg, batch_size=batch_size, lr=lr, mode=mode, seed=seed,
                  sampler=sampler, subgraph_size=subgraph_size, optimizer=optimizer, epochs=epochs,
-                 ahead=ahead)
+                 ahead=ahead, streams=streams)
     k, L = tr.k, tr.L
     metrics = Metrics()
     val_nodes = np.flatnonzero(g.val_mask) if g.val_mask is not None else np.empty(0, dtype=np.int64)
