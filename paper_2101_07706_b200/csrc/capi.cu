@@ -161,6 +161,7 @@ struct skg_gcn {
 // symmetry check: w[j,i] exists and equals w[i,j] bitwise for every stored (i,j)
 __global__ void k_check_symmetric(int64_t n, const int64_t* off, const int32_t* col,
                                   const double* w, int* bad) {
+  SKG_PDL_PROLOGUE();
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     for (int64_t e = off[i] + threadIdx.x; e < off[i + 1]; e += blockDim.x) {
       int j = col[e];
@@ -180,6 +181,7 @@ __global__ void k_check_symmetric(int64_t n, const int64_t* off, const int32_t* 
 // normalised-graph check: w[e] == 1.0/sqrt(d_i * d_j) bit for bit (graph.py:180-182)
 __global__ void k_check_normalized(int64_t n, const int64_t* off, const int32_t* col,
                                    const double* w, double* degd, int* bad) {
+  SKG_PDL_PROLOGUE();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     degd[i] = (double)(off[i + 1] - off[i]);
@@ -187,6 +189,7 @@ __global__ void k_check_normalized(int64_t n, const int64_t* off, const int32_t*
 }
 __global__ void k_check_normalized2(int64_t n, const int64_t* off, const int32_t* col,
                                     const double* w, const double* degd, int* bad) {
+  SKG_PDL_PROLOGUE();
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     for (int64_t e = off[i] + threadIdx.x; e < off[i + 1]; e += blockDim.x) {
       const double x = __ddiv_rn(1.0, __dsqrt_rn(__dmul_rn(degd[i], degd[col[e]])));
@@ -196,6 +199,7 @@ __global__ void k_check_normalized2(int64_t n, const int64_t* off, const int32_t
 }
 
 __global__ void k_ids64_to_32(const int64_t* in, int64_t n, int32_t* out) {
+  SKG_PDL_PROLOGUE();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)in[i];
 }
@@ -890,6 +894,7 @@ extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, in
 }
 
 __global__ void k_ledger_add(const PlanDev* plans, int L, int64_t* ledger) {
+  SKG_PDL_PROLOGUE();
   const PlanDev& P = plans[blockIdx.x];
   for (int t = threadIdx.x; t < L; t += blockDim.x) {
     // reference layer order is bottom-up: layer l <-> top-down t = L-1-l (LADIES);
@@ -910,7 +915,7 @@ extern "C" int skg_plans_ledger_add(skg_plans* ps, int slot0, int n, uint64_t le
                                     void* stream) {
   ARG(ps && slot0 >= 0 && n >= 1 && slot0 + n <= ps->n_slots && ledger_dev, "bad ledger arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  LAUNCH_NAMED("k_ledger_add", st, k_ledger_add<<<n, 32, 0, st>>>(ps->d_plans + slot0, ps->L, (int64_t*)ledger_dev));
+  launch_k("k_ledger_add", st, dim3(n), dim3(32), 0, k_ledger_add, ps->d_plans + slot0, ps->L, (int64_t*)ledger_dev);
   CK(cudaGetLastError());
   return SKG_OK;
 }

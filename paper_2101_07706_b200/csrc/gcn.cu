@@ -79,6 +79,7 @@ static int row_blocks(int max_rows, int n) {
 // X0[slot][c] = X[S_0[c]] from the owner's shard (local or NVLink peer pointer).
 template <typename T>
 __global__ void k_gather_b(FeatStore fs, const SlotDesc* sd, Act<T> out) {
+  SKG_PDL_PROLOGUE();
   const SlotDesc d = sd[blockIdx.y];
   const int n = *d.n_in;
   T* o = out.at(blockIdx.y);
@@ -96,7 +97,7 @@ __global__ void k_gather_b(FeatStore fs, const SlotDesc* sd, Act<T> out) {
 template <typename T>
 void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows, Act<T> out,
                    cudaStream_t st) {
-  LAUNCH_NAMED("k_gather_b", st, k_gather_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(fs, sd, out));
+  launch_k("k_gather_b", st, dim3(dim3(row_blocks(max_rows, n), n)), dim3(256), 0, k_gather_b<T>, fs, sd, out);
 }
 
 // ------------------------------------------------------------------ SpMM (K8 / K10)
@@ -115,6 +116,7 @@ __device__ __forceinline__ void store_split(const Vec4<double>&, double*, double
 template <typename T, bool TRANS, bool RELU>
 __global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, T* out_lo,
                          int max_rows, int64_t width) {
+  SKG_PDL_PROLOGUE();
   const LayerDesc d = lds[blockIdx.y];
   const int rows = TRANS ? *d.cols : *d.rows;
   const int32_t* __restrict__ ip = TRANS ? d.tindptr : d.indptr;
@@ -155,9 +157,9 @@ template <typename T>
 void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
             Act<T> H, Act<T> out, T* out_lo, int64_t width, cudaStream_t st) {
   dim3 grid(row_blocks(max_rows, n), n);
-  if (transposed) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, true, false><<<grid, 256, 0, st>>>(ld, A, H, out, out_lo, max_rows, width)));
-  else if (relu_in) LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, true><<<grid, 256, 0, st>>>(ld, A, H, out, out_lo, max_rows, width)));
-  else LAUNCH_NAMED("k_spmm_b", st, (k_spmm_b<T, false, false><<<grid, 256, 0, st>>>(ld, A, H, out, out_lo, max_rows, width)));
+  if (transposed) launch_k("k_spmm_b", st, dim3(grid), dim3(256), 0, k_spmm_b<T, true, false>, ld, A, H, out, out_lo, max_rows, width);
+  else if (relu_in) launch_k("k_spmm_b", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, true>, ld, A, H, out, out_lo, max_rows, width);
+  else launch_k("k_spmm_b", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, false>, ld, A, H, out, out_lo, max_rows, width);
 }
 
 // full-graph SpMM for predict_logits (int64 offsets)
@@ -165,6 +167,7 @@ template <typename T, bool RELU>
 __global__ void k_spmm_full(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ col,
                             const double* __restrict__ w, const T* __restrict__ A, int64_t lda,
                             T* __restrict__ out, int64_t ldo, int64_t width) {
+  SKG_PDL_PROLOGUE();
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
@@ -186,9 +189,9 @@ void spmm_full(int64_t n, const int64_t* off, const int32_t* col, const double* 
                int64_t lda, bool relu_in, T* out, int64_t ldo, int64_t width, cudaStream_t st) {
   int blocks = 16 * sms();
   if (relu_in)
-    LAUNCH_NAMED("k_spmm_full", st, (k_spmm_full<T, true><<<blocks, 256, 0, st>>>(n, off, col, w, A, lda, out, ldo, width)));
+    launch_k("k_spmm_full", st, dim3(blocks), dim3(256), 0, k_spmm_full<T, true>, n, off, col, w, A, lda, out, ldo, width);
   else
-    LAUNCH_NAMED("k_spmm_full", st, (k_spmm_full<T, false><<<blocks, 256, 0, st>>>(n, off, col, w, A, lda, out, ldo, width)));
+    launch_k("k_spmm_full", st, dim3(blocks), dim3(256), 0, k_spmm_full<T, false>, n, off, col, w, A, lda, out, ldo, width);
 }
 
 // ------------------------------------------------------------------ GEMM (K9)
@@ -198,6 +201,7 @@ template <typename T, bool TA, bool TB, int BM, int BN, int BK, int TM, int TN>
 __global__ void __launch_bounds__((BM / TM) * (BN / TN))
     k_gemm_b(int Mfix, int N, int Kfix, const int32_t* const* dM, const int32_t* const* dK,
              Act<T> A, Act<T> B, Act<T> C, int accumulate) {
+  SKG_PDL_PROLOGUE();
   constexpr int NT = (BM / TM) * (BN / TN);
   const int z = blockIdx.z;
   const int M = dM ? *dM[z] : Mfix;
@@ -272,10 +276,10 @@ static void gemm_launch(bool ta, bool tb, int n, int M, int N, int K, const int3
                         cudaStream_t st) {
   constexpr int NT = (BM / TM) * (BN / TN);
   dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM, n);
-  if (!ta && !tb) LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, false, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
-  else if (ta && !tb) LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, true, false, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
-  else if (!ta && tb) LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, false, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
-  else LAUNCH_NAMED("k_gemm_b", st, (k_gemm_b<T, true, true, BM, BN, BK, TM, TN><<<grid, NT, 0, st>>>(M, N, K, dM, dK, A, B, C, acc)));
+  if (!ta && !tb) launch_k("k_gemm_b", st, dim3(grid), dim3(NT), 0, k_gemm_b<T, false, false, BM, BN, BK, TM, TN>, M, N, K, dM, dK, A, B, C, acc);
+  else if (ta && !tb) launch_k("k_gemm_b", st, dim3(grid), dim3(NT), 0, k_gemm_b<T, true, false, BM, BN, BK, TM, TN>, M, N, K, dM, dK, A, B, C, acc);
+  else if (!ta && tb) launch_k("k_gemm_b", st, dim3(grid), dim3(NT), 0, k_gemm_b<T, false, true, BM, BN, BK, TM, TN>, M, N, K, dM, dK, A, B, C, acc);
+  else launch_k("k_gemm_b", st, dim3(grid), dim3(NT), 0, k_gemm_b<T, true, true, BM, BN, BK, TM, TN>, M, N, K, dM, dK, A, B, C, acc);
 }
 
 int g_gemm_mode = 3;  // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
@@ -309,6 +313,7 @@ void gemm_plain(int M, int N, int K, const T* A, int64_t lda, const T* B, int64_
 template <typename T>
 __global__ void k_reduce_slots(const T* parts, int64_t pstride, int n, int64_t rows, int64_t cols,
                                int64_t ldp, T* C, int64_t ldc, int accumulate) {
+  SKG_PDL_PROLOGUE();
   const int64_t total = rows * cols;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -324,8 +329,8 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
                   int64_t ldp, T* C, int64_t ldc, bool accumulate, cudaStream_t st) {
   int64_t total = rows * cols;
   int blocks = (int)std::min<int64_t>((total + 255) / 256, 8 * sms());
-  LAUNCH_NAMED("k_reduce_slots", st, (k_reduce_slots<T><<<std::max(blocks, 1), 256, 0, st>>>(parts, part_stride, n, rows, cols,
-                                                                 ldp, C, ldc, accumulate)));
+  launch_k("k_reduce_slots", st, dim3(std::max(blocks, 1)), dim3(256), 0, k_reduce_slots<T>, parts, part_stride, n, rows, cols,
+                                                                 ldp, C, ldc, accumulate);
 }
 
 // ------------------------------------------------------------------ softmax CE (K11)
@@ -334,6 +339,7 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
 template <typename T>
 __global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T> Z, int C,
                                Act<T> G, T* G_lo, int max_rows, double* row_loss, int64_t rl_stride) {
+  SKG_PDL_PROLOGUE();
   const SlotDesc d = sd[blockIdx.y];
   const int n = *d.n_batch;
   __shared__ int s_nlab;
@@ -395,6 +401,7 @@ __global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T>
 
 __global__ void k_loss_mean(const SlotDesc* sd, const int32_t* labels, const double* row_loss,
                             int64_t rl_stride, double* loss_out) {
+  SKG_PDL_PROLOGUE();
   const SlotDesc d = sd[blockIdx.x];
   const int n = *d.n_batch;
   typedef cub::BlockReduce<double, 256> BRD;
@@ -421,9 +428,8 @@ __global__ void k_loss_mean(const SlotDesc* sd, const int32_t* labels, const dou
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
                   Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st) {
-  LAUNCH_NAMED("k_softmax_ce_b", st, (k_softmax_ce_b<T><<<dim3(row_blocks(max_rows, n), n), 256, 0, st>>>(
-      sd, labels, Z, C, G, G_lo, max_rows, row_loss, max_rows)));
-  LAUNCH_NAMED("k_loss_mean", st, (k_loss_mean<<<n, 256, 0, st>>>(sd, labels, row_loss, max_rows, loss_out)));
+  launch_k("k_softmax_ce_b", st, dim3(dim3(row_blocks(max_rows, n), n)), dim3(256), 0, k_softmax_ce_b<T>, sd, labels, Z, C, G, G_lo, max_rows, row_loss, max_rows);
+  launch_k("k_loss_mean", st, dim3(n), dim3(256), 0, k_loss_mean, sd, labels, row_loss, max_rows, loss_out);
 }
 
 // ------------------------------------------------------------------ optimizers (K12 epilogue)
@@ -443,6 +449,7 @@ template <> __device__ __forceinline__ double ad(double a, double b) { return __
 // training.py:402-404 with the average of training.py:506: w -= lr * (g / contributors)
 template <typename T>
 __global__ void k_sgd(T* w, const T* g, int64_t n, T lr, T contrib) {
+  SKG_PDL_PROLOGUE();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     w[i] = ad(w[i], -ml(lr, dv(g[i], contrib)));
 }
@@ -451,6 +458,7 @@ __global__ void k_sgd(T* w, const T* g, int64_t n, T lr, T contrib) {
 template <typename T>
 __global__ void k_adam(T* w, const T* g, T* m, T* v, int64_t n, T lr, T contrib, T b1, T b2,
                        T omb1, T omb2, T bc1, T bc2, T eps) {
+  SKG_PDL_PROLOGUE();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     T gr = dv(g[i], contrib);
     T mi = ad(ml(m[i], b1), ml(omb1, gr));
@@ -465,7 +473,7 @@ __global__ void k_adam(T* w, const T* g, T* m, T* v, int64_t n, T lr, T contrib,
 template <typename T>
 void sgd_step(T* w, const T* g, int64_t n, double lr, double contrib, cudaStream_t st) {
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * sms());
-  LAUNCH_NAMED("k_sgd", st, k_sgd<T><<<std::max(blocks, 1), 256, 0, st>>>(w, g, n, (T)lr, (T)contrib));
+  launch_k("k_sgd", st, dim3(std::max(blocks, 1)), dim3(256), 0, k_sgd<T>, w, g, n, (T)lr, (T)contrib);
 }
 
 template <typename T>
@@ -473,19 +481,20 @@ void adam_step(T* w, const T* g, T* m, T* v, int64_t n, double lr, double contri
                double b2, double omb1, double omb2, double bc1, double bc2, double eps,
                cudaStream_t st) {
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * sms());
-  LAUNCH_NAMED("k_adam", st, k_adam<T><<<std::max(blocks, 1), 256, 0, st>>>(w, g, m, v, n, (T)lr, (T)contrib, (T)b1, (T)b2,
-                                                         (T)omb1, (T)omb2, (T)bc1, (T)bc2, (T)eps));
+  launch_k("k_adam", st, dim3(std::max(blocks, 1)), dim3(256), 0, k_adam<T>, w, g, m, v, n, (T)lr, (T)contrib, (T)b1, (T)b2,
+                                                         (T)omb1, (T)omb2, (T)bc1, (T)bc2, (T)eps);
 }
 
 template <typename T>
 __global__ void k_zero(T* p, int64_t n) {
+  SKG_PDL_PROLOGUE();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = T(0);
 }
 template <typename T>
 void fill_zero(T* p, int64_t n, cudaStream_t st) {
   if (n <= 0) return;
   int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * sms());
-  LAUNCH_NAMED("k_zero", st, k_zero<T><<<std::max(blocks, 1), 256, 0, st>>>(p, n));
+  launch_k("k_zero", st, dim3(std::max(blocks, 1)), dim3(256), 0, k_zero<T>, p, n);
 }
 
 #define INST(T)                                                                                     \

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ TcMaps maps, int Mfix, int N, int Kfix,
               const int32_t* const* dM, const int32_t* const* dK, int a_slots, int b_slots,
               Act<float> C, int accumulate) {
+  SKG_PDL_PROLOGUE();
   using namespace tc;
   using CF = Cfg<BN, MODE>;
   constexpr bool SPLIT = MODE == 3;
@@ -414,7 +415,7 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
   }
   dim3 grid((N + BN - 1) / BN, (M + tc::BM - 1) / tc::BM, n);
   const int as = A.stride ? n : 1, bs = B.stride ? n : 1;
-  LAUNCH_NAMED("k_gemm_tc", st, kern<<<grid, tc::NTHREADS, CF::SMEM, st>>>(maps, M, N, K, dM, dK, as, bs, C, acc ? 1 : 0));
+  launch_k("k_gemm_tc", st, dim3(grid), dim3(tc::NTHREADS), CF::SMEM, kern, maps, M, N, K, dM, dK, as, bs, C, acc ? 1 : 0);
   return SKG_OK;
 }
 
@@ -448,6 +449,7 @@ int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_
 // outputs (row stride ld_out); padding columns are written as zero
 __global__ void k_split_tf32(const float* __restrict__ in, int64_t ld_in, int64_t rows, int64_t cols,
                              float* __restrict__ hi, float* __restrict__ lo, int64_t ld_out) {
+  SKG_PDL_PROLOGUE();
   const int64_t total = rows * ld_out;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / ld_out, c = i % ld_out;
@@ -463,11 +465,12 @@ void split_tf32(const float* in, int64_t ld_in, int64_t rows, int64_t cols, floa
   const int64_t total = rows * ld_out;
   if (total <= 0) return;
   const int blocks = (int)std::min<int64_t>((total + 255) / 256, 1184);
-  LAUNCH_NAMED("k_split_tf32", st, (k_split_tf32<<<blocks, 256, 0, st>>>(in, ld_in, rows, cols, hi, lo, ld_out)));
+  launch_k("k_split_tf32", st, dim3(blocks), dim3(256), 0, k_split_tf32, in, ld_in, rows, cols, hi, lo, ld_out);
 }
 
 // all layers' weights in one launch: W_l (d_l x d_{l+1}, dense rows) -> padded hi / lo
 __global__ void k_split_weights(WSplitTable t) {
+  SKG_PDL_PROLOGUE();
   for (int l = 0; l < t.L; ++l) {
     const int64_t rows = t.rows[l], cols = t.cols[l], ldo = t.ld_out[l];
     const float* in = t.w[l];
@@ -486,7 +489,7 @@ __global__ void k_split_weights(WSplitTable t) {
 }
 
 void split_weights(const WSplitTable& t, cudaStream_t st) {
-  LAUNCH_NAMED("k_split_weights", st, (k_split_weights<<<296, 256, 0, st>>>(t)));
+  launch_k("k_split_weights", st, dim3(296), dim3(256), 0, k_split_weights, t);
 }
 
 // test hook: C = op(A) op(B) for host arrays (row-major, ld = inner dim)

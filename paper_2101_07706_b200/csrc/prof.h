@@ -1,20 +1,57 @@
-// Optional per-kernel CUDA-event timing (bench.py's roofline measures the dominant kernel
-// live): when a target name is set, every launch of that kernel is bracketed by events on
-// its own stream.  Off by default (one string compare per launch).
+// Kernel launch helper: every launch of the library goes through launch_k, which
+//  * uses programmatic dependent launch (PDL): the next kernel of a stream may be scheduled
+//    while the current one drains; every kernel starts with SKG_PDL_PROLOGUE(), which
+//    triggers its dependents and then waits for its own predecessor grid to complete, so
+//    stream order and memory visibility are unchanged (off unless SKG_PDL is set);
+//  * brackets the launch with CUDA events on its own stream when bench.py's roofline asks
+//    for that kernel by name (one string compare per launch otherwise).
 #pragma once
 #include <cuda_runtime.h>
 
+#include <utility>
+
 namespace skg {
 extern unsigned long long g_kernel_launches;
+extern int g_pdl;
 bool prof_match(const char* name);
 void prof_record(cudaStream_t st, bool before);
+
+// kernels of the GCN chain (main stream)
+inline bool gcn_kernel(const char* n) {
+  static const char* const names[] = {"k_gemm_tc", "k_gemm_b", "k_gather_b", "k_spmm_b", "k_softmax_ce_b",
+                                      "k_loss_mean", "k_reduce_slots", "k_sgd", "k_adam", "k_split_weights",
+                                      "k_ledger_add", "k_zero"};
+  for (const char* m : names) {
+    const char* a = n;
+    const char* b = m;
+    while (*a && *a == *b) ++a, ++b;
+    if (*a == 0 && *b == 0) return true;
+  }
+  return false;
+}
+
+template <typename... P, typename... A>
+inline void launch_k(const char* name, cudaStream_t st, dim3 grid, dim3 block, size_t smem,
+                     void (*kern)(P...), A&&... args) {
+  const bool pm = prof_match(name);
+  if (pm) prof_record(st, true);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl == 1 || (g_pdl == 2 && gcn_kernel(name));
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+  if (pm) prof_record(st, false);
+  ++g_kernel_launches;
+}
 }  // namespace skg
 
-#define LAUNCH_NAMED(name, st, ...)                  \
-  do {                                               \
-    const bool pm_ = skg::prof_match(name);          \
-    if (pm_) skg::prof_record((st), true);           \
-    __VA_ARGS__;                                     \
-    if (pm_) skg::prof_record((st), false);          \
-    ++skg::g_kernel_launches;                        \
-  } while (0)
+// First statement of every kernel: let the next grid of the stream launch, then wait for
+// the previous one (no-ops when launched without PDL).
+#define SKG_PDL_PROLOGUE() \
+  asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory")
