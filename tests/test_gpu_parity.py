@@ -343,3 +343,30 @@ def test_unnormalised_asymmetric_graph_vs_oracle(seed):
         exp_s = O.saint_plan(og, opart, 1, train, 40, ocfg, 2, np.random.default_rng(seed), norms=norms)
         got_s = pkg.saint_plan(g, part, 1, train, 40, cfg, 2, np.random.default_rng(seed))
         assert_plan_equal(plan_to_dict(got_s), plan_to_dict(exp_s), value_rtol=VAL_RTOL)
+
+
+@pytest.mark.parametrize("normalised", [True, False])
+def test_dense_graph_heavy_contributions_vs_oracle(normalised):
+    """Dense graph: candidates receive up to ~100 contributions, so the light slots (<= 4),
+    the 8-lane and warp heavy folds (5..32) and the CTA fold (> 32) all run; with stored
+    (non-normalised, asymmetric) weights the slot/overflow weight copies are used too."""
+    pkg = P()
+    r = np.random.default_rng(4242 + int(normalised))
+    n = 400
+    m = 40000
+    u, v = r.integers(0, n, m), r.integers(0, n, m)
+    og = O.normalize_weights(O.graph_from_edge_array(np.stack([u, v], 1), n))
+    if not normalised:
+        og.weights = r.uniform(0.05, 2.0, size=len(og.weights))
+    g = to_pkg_graph(og)
+    k = 2
+    opart = O.partition_nodes(n, k, "random", seed=3)
+    part = pkg.Partition(n_workers=k, owner=opart.owner)
+    for mode, D in (("full", 0.0), ("skewed", 8.0), ("local", 0.0)):
+        for budget in (16, 128):
+            ocfg = O.SamplerConfig(budget=budget, skew_constant=D, mode=mode)
+            cfg = pkg.SamplerConfig(budget=budget, skew_constant=D, mode=mode)
+            batch = opart.owned_by(0)[:180]
+            exp = O.ladies_plan(og, opart, 0, batch, ocfg, 3, np.random.default_rng(11))
+            got = pkg.ladies_plan(g, part, 0, batch, cfg, 3, np.random.default_rng(11))
+            assert_plan_equal(plan_to_dict(got), plan_to_dict(exp), value_rtol=VAL_RTOL)
