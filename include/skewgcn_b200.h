@@ -116,6 +116,11 @@ int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* workers,
                              const uint64_t* rng_states, void* stream);
 /* SAINT candidate set (sorted training nodes).  precompute != 0 caches
  * train_column_norms (training.py:211-213) used by full / skewed modes. */
+// column_norms(g, rows, candidates) for large row sets: pull formulation (ordered fold over
+// each candidate's column, i ascending).  Replaces graph.py:198-220 when |rows| is large
+// (GraphSAINT's training-set norms, training.py:211-213).  out: host double[n_cand].
+int skg_column_norms_pull(skg_ctx* ctx, const int64_t* rows, int64_t n_rows, const int64_t* cand,
+                          int64_t n_cand, double* out);
 int skg_saint_set_candidates(skg_plans* ps, const int64_t* train_ids, int64_t n_train,
                              int precompute, void* stream);
 /* saint_plan for slots [0, n) with subgraph size = budget (<= |candidates| assumed). */

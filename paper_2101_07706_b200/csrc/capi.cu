@@ -786,6 +786,64 @@ extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* wor
                        (int)ps->budget, st);
 }
 
+// column_norms(g, rows, candidates) (graph.py:198-220) by the pull formulation: for each
+// candidate j an ordered fold over column j (i ascending, == the np.add.at order) of w_ij^2
+// for i in `rows`.  Used for large row sets (GraphSAINT's training set), where the push
+// (LADIES expand) form would need a plan per call.
+extern "C" int skg_column_norms_pull(skg_ctx* c, const int64_t* rows, int64_t n_rows,
+                                     const int64_t* cand, int64_t n_cand, double* out) {
+  ARG(c && rows && cand && out && n_rows >= 1 && n_cand >= 0, "bad column-norm arguments");
+  ARG(n_rows < (1LL << 31) && n_cand < (1LL << 31), "node set too large");
+  CK(cudaSetDevice(c->device));
+  if (n_cand == 0) return SKG_OK;
+  std::vector<int32_t> r32(n_rows), c32(n_cand);
+  for (int64_t i = 0; i < n_rows; ++i) {
+    ARG(rows[i] >= 0 && rows[i] < c->n, "node id out of range for this graph");
+    ARG(i == 0 || rows[i] > rows[i - 1], "node set must be strictly increasing");
+    r32[i] = (int32_t)rows[i];
+  }
+  for (int64_t i = 0; i < n_cand; ++i) {
+    ARG(cand[i] >= 0 && cand[i] < c->n, "node id out of range for this graph");
+    ARG(i == 0 || cand[i] > cand[i - 1], "node set must be strictly increasing");
+    c32[i] = (int32_t)cand[i];
+  }
+  const int n_words = (int)((c->n + 31) / 32);
+  int32_t *d_rows = nullptr, *d_cand = nullptr, *d_err = nullptr;
+  uint32_t* d_bm = nullptr;
+  double* d_out = nullptr;
+  CK(cudaMalloc(&d_rows, 4 * n_rows));
+  CK(cudaMalloc(&d_cand, 4 * n_cand));
+  CK(cudaMalloc(&d_bm, 4 * (size_t)n_words));
+  CK(cudaMalloc(&d_out, 8 * n_cand));
+  CK(cudaMalloc(&d_err, 4));
+  CK(cudaMemset(d_err, 0, 4));
+  CK(cudaMemcpy(d_rows, r32.data(), 4 * n_rows, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(d_cand, c32.data(), 4 * n_cand, cudaMemcpyHostToDevice));
+  launch_set_bitmap(d_rows, (int32_t)n_rows, d_bm, n_words, 0);
+  int rc = launch_pull_norms(c->gdev(), d_cand, (int32_t)n_cand, d_bm, d_out, d_err, 0);
+  int err = 0;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (!rc && e == cudaSuccess) {
+    cudaMemcpy(out, d_out, 8 * n_cand, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&err, d_err, 4, cudaMemcpyDeviceToHost);
+  }
+  cudaFree(d_rows);
+  cudaFree(d_cand);
+  cudaFree(d_bm);
+  cudaFree(d_out);
+  cudaFree(d_err);
+  if (rc) return rc;
+  if (e != cudaSuccess) {
+    set_error(std::string("column norms: ") + cudaGetErrorString(e));
+    return SKG_ERR_CUDA;
+  }
+  if (err & EB_NOT_ADJACENT) {
+    set_error("candidates not adjacent to s_l");
+    return SKG_ERR_NOT_ADJACENT;
+  }
+  return SKG_OK;
+}
+
 extern "C" int skg_saint_set_candidates(skg_plans* ps, const int64_t* train, int64_t n_train,
                                         int precompute, void* stream) {
   ARG(ps && ps->kind == KIND_SAINT, "not a SAINT plan set");

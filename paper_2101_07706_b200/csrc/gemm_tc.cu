@@ -419,12 +419,22 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
   return SKG_OK;
 }
 
+int g_bn_override = 0;  // debug / tuning: force the N tile (32, 64, 128, 256)
+
 template <bool TA, bool TB, int MODE>
-static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
+static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dM2,
                        const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st) {
-  // 64-wide N tiles: the 3xTF32 issue cost per K step is nearly independent of N up to 256,
-  // and narrow tiles put 4x more CTAs on these skinny problems (M = a few thousand rows)
-  if (N <= 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  const int32_t* const* dK = dM2;
+  int bn = g_bn_override;
+  if (!bn) {
+    // 64-wide N tiles put 4x more CTAs on the skinny LADIES problems (M = a few thousand
+    // rows, one wave); once the grid spans several waves, wider tiles amortise the A reads
+    const long long tiles64 = (long long)((M + 127) / 128) * ((N + 63) / 64) * n;
+    bn = N <= 32 ? 32 : (tiles64 > 4 * 148 && N >= 256) ? 256 : (tiles64 > 2 * 148 && N >= 128) ? 128 : 64;
+  }
+  if (bn == 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  if (bn == 128) return launch_tc<TA, TB, 128, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  if (bn == 256) return launch_tc<TA, TB, 256, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
   return launch_tc<TA, TB, 64, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
 }
 
@@ -548,6 +558,11 @@ extern "C" int skg_debug_gemm(int mode, int ta, int tb, int M, int N, int K, con
 }
 
 // debug: time `iters` GEMMs on device-resident (zero) split operands, M x K by K x N
+extern "C" int skg_debug_gemm_bn(int bn) {
+  skg::g_bn_override = bn;
+  return 0;
+}
+
 extern "C" int skg_debug_gemm_timed(int mode, int ta, int tb, int M, int N, int K, int iters,
                                     float* us_out) {
   using namespace skg;

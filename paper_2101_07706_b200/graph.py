@@ -187,6 +187,9 @@ def neighbor_union(g: WeightedGraph, s) -> np.ndarray:
     return one_layer(g, s)["cand"].astype(np.int64)
 
 
+_PUSH_MAX_ROWS = 16384  # row sets above this use the pull formulation
+
+
 def column_norms(g: WeightedGraph, s_l, candidates) -> np.ndarray:
     """sum_{i in s_l} w_ij^2 per candidate, np.add.at order (graph.py:198-220), on the GPU."""
     from ._device import one_layer
@@ -196,6 +199,17 @@ def column_norms(g: WeightedGraph, s_l, candidates) -> np.ndarray:
         if len(candidates):
             raise ValueError("candidates must be empty when s_l is empty")
         return np.zeros(0)
+    if len(s_l) > _PUSH_MAX_ROWS:  # pull formulation: no per-call plan, any row count
+        from ._device import device_graph
+        from ._native import check, lib, ptr
+        import ctypes as C
+        dg = device_graph(g)
+        cand64 = np.ascontiguousarray(candidates, dtype=np.int64)
+        rows64 = np.ascontiguousarray(s_l, dtype=np.int64)
+        out = np.zeros(len(cand64), dtype=np.float64)
+        check(lib.skg_column_norms_pull(dg.ctx, ptr(rows64, C.c_int64), len(rows64),
+                                        ptr(cand64, C.c_int64), len(cand64), ptr(out, C.c_double)))
+        return out
     lay = one_layer(g, s_l)
     cand, norm = lay["cand"].astype(np.int64), lay["norm"]
     pos = np.searchsorted(cand, candidates)

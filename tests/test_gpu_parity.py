@@ -370,3 +370,24 @@ def test_dense_graph_heavy_contributions_vs_oracle(normalised):
             exp = O.ladies_plan(og, opart, 0, batch, ocfg, 3, np.random.default_rng(11))
             got = pkg.ladies_plan(g, part, 0, batch, cfg, 3, np.random.default_rng(11))
             assert_plan_equal(plan_to_dict(got), plan_to_dict(exp), value_rtol=VAL_RTOL)
+
+
+def test_column_norms_pull_large_row_set_vs_oracle():
+    """column_norms over a large row set (> the push path's limit) uses the pull
+    formulation; it must equal the oracle's np.add.at fold bit for bit, and raise the
+    reference's error for non-adjacent candidates."""
+    pkg = P()
+    r = np.random.default_rng(99)
+    n, m = 30000, 150000
+    u, v = r.integers(0, n, m), r.integers(0, n, m)
+    og = O.normalize_weights(O.graph_from_edge_array(np.stack([u, v], 1), n))
+    g = to_pkg_graph(og)
+    rows = np.sort(r.choice(n, 20000, replace=False))
+    cand = O.neighbor_union(og, rows)
+    exp = O.column_norms(og, rows, cand)
+    got = pkg.column_norms(g, rows, cand)
+    assert np.array_equal(got, exp)
+    isolated = np.setdiff1d(np.arange(n), cand)
+    if len(isolated):
+        with pytest.raises(ValueError, match="not adjacent"):
+            pkg.column_norms(g, rows, np.sort(np.concatenate([cand[:5], isolated[:1]])))
