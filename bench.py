@@ -427,7 +427,6 @@ def run_ours(args):
                               "algorithmic_bytes": int(alg_bytes), "duration_ms": round(samp, 4),
                               "plans": T * n_my},
             "e2e": {"value": round(1000.0 * K / e2e_ms, 3), "unit": "iters/s",
-                    "last_loss_sum": host_losses[-1],
                     "h2d_bytes_per_step": int(h2d[0] // K), "d2h_bytes_per_step": 8 * n_my},
             "clocks": clk.summary(),
             "graph_build_s": round(t_gen, 2),
