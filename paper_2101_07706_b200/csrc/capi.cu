@@ -609,6 +609,7 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     cv.add(P.heavy, lad ? cap_cand : 1);
     cv.add(P.huge, lad ? cap_cand : 1);
     cv.add(P.updeg, lad ? cap_rows : 1);
+    cv.add(P.row_any, lad ? cap_rows : 1);
     cv.add(P.cand_cnt, lad ? cap_cand : 1);
     cv.add(P.pair_off, cap_rows + 1);
     cv.add(P.word_prefix, n_words);

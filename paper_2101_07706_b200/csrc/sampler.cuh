@@ -81,6 +81,7 @@ struct PlanDev {
   int32_t* heavy;           // [cap_cand] candidate ranks with count > kSlots
   int32_t* huge;            // [cap_cand] heavy candidates with count > 32
   double* updeg;            // [cap_rows] degree of each upper row (normalised graphs)
+  int32_t* row_any;         // [cap_rows] local mode: the upper row kept a column (range expand)
   int32_t* cand_cnt;        // [cap_cand] contributions per candidate
   int64_t* pair_off;        // [cap_rows+1]
   int32_t* word_prefix;     // [n_words]
@@ -120,6 +121,8 @@ struct PlanDev {
 };
 
 constexpr int kSlots = 4;         // contributions kept per node before overflowing
+constexpr int kRangeNodes = 65536;  // nodes per CTA of the shared-memory-counting expand
+constexpr int kMaxRanges = 16;      // beyond this many ranges per plan: global-atomic expand
 constexpr int kTileWords = 256;    // bitmap words per compaction tile (8 warps x 32 words)
 constexpr int kTileCand = 4096;    // candidates per scan tile
 constexpr int kSmallBucket = 16;   // buckets folded in registers
