@@ -13,6 +13,9 @@ from .graph import (WeightedGraph, adjacency_block, column_norms, from_shaped, g
 from .partition import Partition, partition_nodes
 from .sampling import ProbDist, SampleDraw, SamplerConfig
 from .seeding import pcg64_state, spawn_rng
+from .datasets import (SbmSpec, load_dataset, load_features_csv, load_labels_csv, load_masks_csv,
+                       load_partition_csv, save_dataset, synth_sbm)
+from .experiment import DatasetSpec, ExperimentConfig, load_config, run_experiment, save_config
 from .training import (CommLedger, EvalResult, GcnModel, Metrics, MetricRow, PlanLayer, SamplePlan,
                        Trainer, evaluate, forward, init_model, ladies_plan, loss_and_backward,
                        predict_logits, saint_plan, train_column_norms, train_distributed)
@@ -27,4 +30,7 @@ __all__ = [
     "SamplePlan", "Trainer", "evaluate", "forward", "init_model", "ladies_plan",
     "loss_and_backward", "predict_logits", "saint_plan", "train_column_norms",
     "train_distributed", "set_compute_dtype", "compute_dtype", "kernel_launches",
+    "SbmSpec", "synth_sbm", "load_dataset", "save_dataset", "load_features_csv", "load_labels_csv",
+    "load_masks_csv", "load_partition_csv", "DatasetSpec", "ExperimentConfig", "load_config",
+    "save_config", "run_experiment",
 ]

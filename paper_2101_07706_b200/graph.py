@@ -104,7 +104,8 @@ def _canonical_csr(src: np.ndarray, dst: np.ndarray, n_nodes: int):
 
 def graph_from_edges(edges, n_hint: int | None = None, normalize: bool = True) -> WeightedGraph:
     """Undirected edge list -> graph (each edge in both rows, duplicates collapsed)."""
-    e = np.asarray(list(edges), dtype=np.int64).reshape(-1, 2)
+    e = edges if isinstance(edges, np.ndarray) else np.asarray(list(edges), dtype=np.int64)
+    e = np.asarray(e, dtype=np.int64).reshape(-1, 2)
     n = int(e.max()) + 1 if len(e) else 0
     if n_hint is not None:
         n = max(n, n_hint)
@@ -117,26 +118,10 @@ def graph_from_edges(edges, n_hint: int | None = None, normalize: bool = True) -
 
 
 def load_edge_list(path, n_hint: int | None = None) -> WeightedGraph:
-    """Edge-list text loader with the reference's rules (graph.py:115-149)."""
-    path = Path(path)
-    us, vs = [], []
-    with path.open("r", encoding="utf-8") as fh:
-        for lineno, line in enumerate(fh, start=1):
-            text = line.strip()
-            if not text or text.startswith("#"):
-                continue
-            parts = text.split()
-            if len(parts) != 2:
-                raise ValueError(f"{path}:{lineno}: expected 'u v', got {text!r}")
-            try:
-                u, v = int(parts[0]), int(parts[1])
-            except ValueError as exc:
-                raise ValueError(f"{path}:{lineno}: non-integer node id in {text!r}") from exc
-            if u < 0 or v < 0:
-                raise ValueError(f"{path}:{lineno}: negative node id in {text!r}")
-            us.append(u)
-            vs.append(v)
-    return graph_from_edges(list(zip(us, vs)), n_hint=n_hint, normalize=False)
+    """Edge-list text loader with the reference's rules (graph.py:115-149); vectorised,
+    see datasets.load_edge_list."""
+    from .datasets import load_edge_list as _load
+    return _load(path, n_hint=n_hint)
 
 
 def normalize_weights(g: WeightedGraph) -> WeightedGraph:
