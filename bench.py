@@ -65,11 +65,15 @@ def parse():
     if a.lr <= 0:  # GraphSAINT's 1/p-weighted 4500-node blocks diverge at 0.5 with hidden 512
         a.lr = 0.05 if a.sampler == "saint" else 0.5
     if a.hidden <= 0:
-        a.hidden = 512 if a.shape.startswith("amazon") else DIMS_HIDDEN
+        a.hidden = 512 if a.shape.startswith(("amazon", "youtube")) else DIMS_HIDDEN
     return a
 
 
 def workload_name(args):
+    if args.shape.startswith("youtube"):
+        return (f"{args.shape}-shaped LADIES {args.mode} D={args.D:g}, k={args.workers} workers, "
+                f"batch {args.batch}, budget {args.budget}, {N_LAYERS} layers hidden {args.hidden}, "
+                "multi-label BCE pos_weight 50")
     if args.sampler == "saint":
         return (f"{args.shape}-shaped GraphSAINT {args.mode} D={args.D:g}, k={args.workers} workers, "
                 f"subgraph {args.subgraph}, {N_LAYERS} layers hidden {args.hidden}")
@@ -387,7 +391,10 @@ def run_ours(args):
     out = None
     if rank == 0:
         cpu = None
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and tr.multilabel:
+            cpu = {"value": None, "unavailable": "the reference has no multi-label (BCE) loss; "
+                                                 "no CPU implementation to time"}
+        elif not args.no_cpu_baseline and world == 1:
             norms = None
             if saint and args.mode != "local":  # bit-exact with the oracle's (parity tests)
                 norms = P.train_column_norms(g, np.flatnonzero(sg.train_mask))
@@ -563,7 +570,10 @@ def _ref_task(a):
 
 
 def run_reference(args):
-    """The reference algorithm (oracle port) on the host: each step is one full iteration,
+    """The reference arm; GraphSAINT / LADIES softmax configurations only (the reference
+    has no multi-label loss).
+
+    The reference algorithm (oracle port) on the host: each step is one full iteration,
     its k worker-iterations (plan + forward/backward) run in parallel worker processes
     (fork, copy-on-write graph) on all usable host cores."""
     global _REF_CTX
@@ -571,6 +581,10 @@ def run_reference(args):
     world, rank, local = dist_setup(args)
     if rank != 0:
         return None
+    if args.shape.startswith("youtube"):
+        out = {"impl": "reference", "unavailable": "the reference has no multi-label (BCE) loss"}
+        print(json.dumps(out), flush=True)
+        return out
     from paper_2101_07706_b200.synth import make_shaped_graph
     sg = make_shaped_graph(args.shape, seed=0, device=None)
     _REF_CTX = _oracle_setup(args, sg)

@@ -85,6 +85,9 @@ int skg_ctx_feature_ptr(skg_ctx* ctx, uint64_t* out_ptr, int64_t* out_ld);
  * allocation (exportable with skg_ipc_handle); owned and freed by the ctx. */
 int skg_ctx_shard_upload(skg_ctx* ctx, const void* host_rows, int64_t n_rows,
                          uint64_t* out_dev_ptr);
+// Multi-label targets (extension; no reference implementation):
+// n x ceil(C/64) uint64 multi-hot words, bit k%64 of word k/64 = class k.
+int skg_ctx_set_multilabels(skg_ctx* ctx, const uint64_t* words, int32_t n_classes);
 int skg_ctx_set_labels(skg_ctx* ctx, const int64_t* labels);
 /* Replace the ownership map (Partition.owner) without re-uploading the CSR. */
 int skg_ctx_set_owner(skg_ctx* ctx, int32_t n_workers, const int32_t* owner);
@@ -144,6 +147,9 @@ int skg_plan_layer(skg_plans* ps, int slot, int t, int32_t* nodes, int32_t* indp
  * forward / loss_and_backward (training.py:261-318) on slot `slot`.  dims has
  * n_layers+1 entries; weights are row-major d_l x d_{l+1} device arrays. */
 int skg_gcn_create(skg_plans* ps, int n_layers, const int64_t* dims, int dtype, skg_gcn** out);
+// Loss of the GCN head: 0 = softmax cross-entropy (training.py:293-308, default),
+// 1 = multi-label BCE-with-logits, positive weight pos_weight, mean over rows x classes.
+int skg_gcn_set_loss(skg_gcn* g, int kind, double pos_weight);
 int skg_gcn_destroy(skg_gcn* g);
 /* forward + loss + backward; grads (device) += or = dW_l; loss_dev: one double. */
 int skg_gcn_step(skg_gcn* g, int slot, const uint64_t* weight_ptrs, const uint64_t* grad_ptrs,

@@ -35,6 +35,18 @@ def current_stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
+def pack_multihot(y: np.ndarray) -> np.ndarray:
+    """n x C 0/1 matrix -> n x ceil(C/64) uint64 words (bit k%64 of word k/64 = class k)."""
+    y = np.asarray(y) != 0
+    n, c = y.shape
+    nw = (c + 63) // 64
+    pad = np.zeros((n, nw * 64), dtype=bool)
+    pad[:, :c] = y
+    weight = np.left_shift(np.uint64(1), np.arange(64, dtype=np.uint64))
+    return np.ascontiguousarray((pad.reshape(n, nw, 64).astype(np.uint64) * weight).sum(axis=2,
+                                                                                      dtype=np.uint64))
+
+
 class PlanSet:
     """One skg_plans arena (n_slots plans) and its GCN workspaces."""
 
@@ -172,11 +184,17 @@ class DeviceGraph:
         return int(ld.value)
 
     def ensure_labels(self, labels: np.ndarray) -> None:
+        """Class per node (1-D, -1 = unlabeled), or an n x C multi-hot matrix for the
+        multi-label BCE loss (packed into 64-bit words per node)."""
         key = (id(labels), labels.__array_interface__["data"][0], labels.shape)
         if key == self.lab_key:
             return
-        l64 = np.ascontiguousarray(labels, dtype=np.int64)
-        check(lib.skg_ctx_set_labels(self.ctx, ptr(l64, C.c_int64)))
+        if labels.ndim == 2:
+            words = pack_multihot(labels)
+            check(lib.skg_ctx_set_multilabels(self.ctx, ptr(words, C.c_uint64), labels.shape[1]))
+        else:
+            l64 = np.ascontiguousarray(labels, dtype=np.int64)
+            check(lib.skg_ctx_set_labels(self.ctx, ptr(l64, C.c_int64)))
         self.lab_key, self.lab_ref = key, labels
 
     # -- plan-set pool ----------------------------------------------------

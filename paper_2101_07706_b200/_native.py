@@ -55,6 +55,8 @@ _sig("skg_ctx_set_feature_map", C.c_int, vp, C.c_int, P(u64), P(i32), P(i32))
 _sig("skg_ctx_feature_ptr", C.c_int, vp, P(u64), P(i64))
 _sig("skg_ctx_shard_upload", C.c_int, vp, vp, i64, P(u64))
 _sig("skg_ctx_set_labels", C.c_int, vp, P(i64))
+_sig("skg_ctx_set_multilabels", C.c_int, vp, P(C.c_uint64), C.c_int32)
+_sig("skg_gcn_set_loss", C.c_int, vp, C.c_int, C.c_double)
 _sig("skg_ctx_info", C.c_int, vp, P(i64))
 _sig("skg_ctx_set_owner", C.c_int, vp, i32, P(i32))
 _sig("skg_plans_ledger_add", C.c_int, vp, C.c_int, C.c_int, u64, vp)
@@ -93,7 +95,7 @@ EXPORTED = [
     "skg_profile_start", "skg_profile_stop",
     "skg_spawn_pcg64", "skg_choice_noreplace", "skg_iteration_inputs", "skg_ctx_create",
     "skg_ctx_destroy", "skg_ctx_set_features", "skg_ctx_set_feature_map", "skg_ctx_feature_ptr", "skg_ctx_shard_upload",
-    "skg_ctx_set_labels", "skg_ctx_set_owner", "skg_ctx_info", "skg_plans_ledger_add", "skg_ipc_handle", "skg_ipc_open", "skg_ipc_close",
+    "skg_ctx_set_labels", "skg_ctx_set_multilabels", "skg_gcn_set_loss", "skg_ctx_set_owner", "skg_ctx_info", "skg_plans_ledger_add", "skg_ipc_handle", "skg_ipc_open", "skg_ipc_close",
     "skg_plans_create", "skg_plans_destroy", "skg_ladies_sample", "skg_ladies_sample_device", "skg_saint_set_candidates", "skg_column_norms_pull",
     "skg_saint_sample", "skg_plan_stats", "skg_plan_layer", "skg_gcn_create", "skg_gcn_destroy",
     "skg_gcn_step", "skg_gcn_step_batch", "skg_gcn_forward", "skg_gcn_read_logits", "skg_predict_logits",

@@ -71,6 +71,9 @@ struct skg_ctx {
   int64_t F = 0, ldx = 0, x_rows = 0;
   int dtype = DT_F32;
   int32_t* d_labels = nullptr;
+  // multi-label targets (multi-hot, y_words 64-bit words per node) for the BCE loss
+  uint64_t* d_ymulti = nullptr;
+  int32_t y_words = 0, y_classes = 0;
   int n_ranks = 1;
   uint64_t* d_shards = nullptr;
   int32_t* d_node_rank = nullptr;
@@ -150,6 +153,8 @@ struct skg_gcn {
   std::vector<int64_t> ldw;
   char* G0lo = nullptr;
   char* parts = nullptr;  // split-K partials of dW, one d_l x d_{l+1} block per slot
+  int loss_kind = 0;      // 0: softmax cross-entropy (training.py:293-308); 1: multi-label BCE
+  double pos_weight = 1.0;
   int64_t part_elems = 0;
   double* row_loss = nullptr;
   LayerDesc* d_layers = nullptr;      // [L][n_slots]
@@ -382,6 +387,7 @@ extern "C" int skg_ctx_destroy(skg_ctx* c) {
   cudaFree(c->d_degd);
   cudaFree(c->d_x);
   cudaFree(c->d_labels);
+  cudaFree(c->d_ymulti);
   cudaFree(c->d_shards);
   cudaFree(c->d_node_rank);
   cudaFree(c->d_node_row);
@@ -465,6 +471,19 @@ extern "C" int skg_ctx_set_labels(skg_ctx* c, const int64_t* labels) {
   cudaFree(c->d_labels);
   CK(cudaMalloc(&c->d_labels, sizeof(int32_t) * std::max<int64_t>(c->n, 1)));
   if (c->n) CK(cudaMemcpy(c->d_labels, l32.data(), sizeof(int32_t) * c->n, cudaMemcpyHostToDevice));
+  return SKG_OK;
+}
+
+// multi-hot targets for the multi-label (BCE) loss: n x words uint64, bit k of word k/64
+extern "C" int skg_ctx_set_multilabels(skg_ctx* c, const uint64_t* words, int32_t n_classes) {
+  ARG(c && words && n_classes >= 1, "bad multi-labels");
+  CK(cudaSetDevice(c->device));
+  const int32_t nw = (n_classes + 63) / 64;
+  cudaFree(c->d_ymulti);
+  CK(cudaMalloc(&c->d_ymulti, sizeof(uint64_t) * nw * std::max<int64_t>(c->n, 1)));
+  if (c->n) CK(cudaMemcpy(c->d_ymulti, words, sizeof(uint64_t) * nw * c->n, cudaMemcpyHostToDevice));
+  c->y_words = nw;
+  c->y_classes = n_classes;
   return SKG_OK;
 }
 
@@ -1146,6 +1165,15 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   return SKG_OK;
 }
 
+// loss of the GCN head: 0 softmax cross-entropy, 1 multi-label BCE-with-logits with
+// positive-class weight pos_weight (mean over rows x classes)
+extern "C" int skg_gcn_set_loss(skg_gcn* g, int kind, double pos_weight) {
+  ARG(g && (kind == 0 || kind == 1) && pos_weight > 0.0, "bad loss");
+  g->loss_kind = kind;
+  g->pos_weight = pos_weight;
+  return SKG_OK;
+}
+
 extern "C" int skg_gcn_destroy(skg_gcn* g) {
   if (!g) return SKG_OK;
   cudaFree(g->arena);
@@ -1255,8 +1283,17 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
   Act<T> G = act<T>(g->G0, R, g->ld_max, g->ld[L], z0);
   Act<T> Gu = act<T>(g->G1, R, g->ld_max, g->ld[L], z0);
   T* G_lo = F32 ? lo_of(g->G0lo, g->ld_max) : nullptr;
-  softmax_ce_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
-                  (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, loss, st);
+  if (g->loss_kind == 1) {
+    if (!c->d_ymulti || c->y_classes != g->dims[L]) {
+      set_error("multi-label BCE needs multi-hot labels with one bit per output class");
+      return SKG_ERR_ARG;
+    }
+    bce_b<T>(g->d_slots + z0, n, Ri, c->d_ymulti, c->y_words, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
+             (int)g->dims[L], g->pos_weight, G, G_lo, g->row_loss + (size_t)z0 * R, loss, st);
+  } else {
+    softmax_ce_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
+                    (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, loss, st);
+  }
   for (int l = L - 1; l >= 0; --l) {
     const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
     const int32_t* const* rows = g->d_rows + (size_t)l * S + z0;
@@ -1318,7 +1355,7 @@ int gcn_dispatch(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* 
 extern "C" int skg_gcn_step(skg_gcn* g, int slot, const uint64_t* wp, const uint64_t* gp,
                             int accumulate, uint64_t loss_dev, void* stream) {
   ARG(g && slot >= 0 && slot < g->n_slots && wp && gp && loss_dev, "bad gcn_step arguments");
-  ARG(g->ps->ctx->d_labels, "labels not set");
+  ARG(g->ps->ctx->d_labels || g->ps->ctx->d_ymulti, "labels not set");
   CK(cudaSetDevice(g->ps->ctx->device));
   return gcn_dispatch(g, slot, 1, wp, gp, accumulate != 0, (double*)loss_dev, true,
                       (cudaStream_t)stream);
@@ -1329,7 +1366,7 @@ extern "C" int skg_gcn_step_batch(skg_gcn* g, int slot0, int n, const uint64_t* 
                                   void* stream) {
   ARG(g && slot0 >= 0 && n >= 1 && slot0 + n <= g->n_slots && wp && gp && loss_dev,
       "bad gcn_step_batch arguments");
-  ARG(g->ps->ctx->d_labels, "labels not set");
+  ARG(g->ps->ctx->d_labels || g->ps->ctx->d_ymulti, "labels not set");
   CK(cudaSetDevice(g->ps->ctx->device));
   return gcn_dispatch(g, slot0, n, wp, gp, accumulate != 0, (double*)loss_dev, true,
                       (cudaStream_t)stream);

@@ -432,6 +432,79 @@ void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels
   launch_k("k_loss_mean", st, dim3(n), dim3(256), 0, k_loss_mean, sd, labels, row_loss, max_rows, loss_out);
 }
 
+// ------------------------------------------------------------------ multi-label BCE
+// torch.nn.BCEWithLogitsLoss(pos_weight=pw, reduction="mean") semantics over the batch rows:
+// l = pw*y*softplus(-z) + (1-y)*softplus(z), dl/dz = sigmoid(z)*(pw*y + 1 - y) - pw*y, both
+// divided by rows*C; warp per row, row sums in fp64, fixed-order mean per slot.
+template <typename T>
+__global__ void k_bce_b(const SlotDesc* sd, const uint64_t* y, int y_words, Act<T> Z, int C, double pw,
+                        Act<T> G, T* G_lo, int max_rows, double* row_loss, int64_t rl_stride) {
+  SKG_PDL_PROLOGUE();
+  const SlotDesc d = sd[blockIdx.y];
+  const int n = *d.n_batch;
+  const T* z0 = Z.at(blockIdx.y);
+  T* g0 = G.at(blockIdx.y);
+  T* gl0 = G_lo ? G_lo + (int64_t)blockIdx.y * G.stride : nullptr;
+  double* rl = row_loss + blockIdx.y * rl_stride;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const double scale = n > 0 ? 1.0 / ((double)n * C) : 0.0;
+  const int rows_all = gl0 ? max_rows : n;  // split output: zero rows past the batch
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows_all; r += nw) {
+    T* g = g0 + (int64_t)r * G.ld;
+    T* gl = gl0 ? gl0 + (int64_t)r * G.ld : nullptr;
+    if (r >= n) {
+      for (int k = lane; k < C; k += 32) g[k] = gl[k] = T(0);
+      continue;
+    }
+    const uint64_t* yr = y + (int64_t)d.batch[r] * y_words;
+    const T* z = z0 + (int64_t)r * Z.ld;
+    double ls = 0.0;
+    for (int k = lane; k < C; k += 32) {
+      const double yk = (double)((yr[k >> 6] >> (k & 63)) & 1ull);
+      const double zk = (double)z[k];
+      const double e = exp(-fabs(zk));
+      const double sp_pos = log1p(e) + fmax(-zk, 0.0);  // softplus(-z) = -log sigmoid(z)
+      const double sp_neg = log1p(e) + fmax(zk, 0.0);   // softplus(z)  = -log(1 - sigmoid(z))
+      ls += pw * yk * sp_pos + (1.0 - yk) * sp_neg;
+      const double sig = zk >= 0.0 ? 1.0 / (1.0 + e) : e / (1.0 + e);
+      const T v = (T)((sig * (pw * yk + 1.0 - yk) - pw * yk) * scale);
+      if (gl) {
+        const float h = tf32_rna((float)v);
+        g[k] = (T)h;
+        gl[k] = (T)tf32_rna((float)v - h);
+      } else {
+        g[k] = v;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(FULLM, ls, o);
+    if (lane == 0) rl[r] = ls;
+  }
+}
+
+__global__ void k_bce_mean(const SlotDesc* sd, const double* row_loss, int64_t rl_stride, int C,
+                           double* loss_out) {
+  SKG_PDL_PROLOGUE();
+  const SlotDesc d = sd[blockIdx.x];
+  const int n = *d.n_batch;
+  typedef cub::BlockReduce<double, 256> BRD;
+  __shared__ typename BRD::TempStorage td;
+  double s = 0.0;
+  const double* rl = row_loss + blockIdx.x * rl_stride;
+  for (int r = threadIdx.x; r < n; r += blockDim.x) s += rl[r];  // fixed assignment
+  const double tot = BRD(td).Sum(s);
+  if (threadIdx.x == 0) loss_out[blockIdx.x] = n ? tot / ((double)n * C) : 0.0;
+}
+
+template <typename T>
+void bce_b(const SlotDesc* sd, int n, int max_rows, const uint64_t* y, int y_words, Act<T> Z, int C,
+           double pos_weight, Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st) {
+  launch_k("k_bce_b", st, dim3(row_blocks(max_rows, n), n), dim3(256), 0, k_bce_b<T>, sd, y, y_words, Z, C,
+           pos_weight, G, G_lo, max_rows, row_loss, (int64_t)max_rows);
+  launch_k("k_bce_mean", st, dim3(n), dim3(256), 0, k_bce_mean, sd, row_loss, (int64_t)max_rows, C, loss_out);
+}
+
 // ------------------------------------------------------------------ optimizers (K12 epilogue)
 template <typename T>
 __device__ __forceinline__ T dv(T a, T b);
@@ -507,6 +580,8 @@ void fill_zero(T* p, int64_t n, cudaStream_t st) {
                                 bool, cudaStream_t);                                                \
   template void softmax_ce_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>, T*, \
                                 double*, double*, cudaStream_t);                                    \
+  template void bce_b<T>(const SlotDesc*, int, int, const uint64_t*, int, Act<T>, int, double, Act<T>, \
+                         T*, double*, double*, cudaStream_t);                                       \
   template void sgd_step<T>(T*, const T*, int64_t, double, double, cudaStream_t);                   \
   template void adam_step<T>(T*, const T*, T*, T*, int64_t, double, double, double, double, double, \
                              double, double, double, double, cudaStream_t);                         \

@@ -103,6 +103,11 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
                   Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st);
+// multi-label BCE-with-logits (pos_weight on positives), mean over rows x C; multi-hot
+// targets y (y_words 64-bit words per node); G (+ TF32 G_lo, tail rows zeroed)
+template <typename T>
+void bce_b(const SlotDesc* sd, int n, int max_rows, const uint64_t* y, int y_words, Act<T> Z, int C,
+           double pos_weight, Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st);
 template <typename T>
 void sgd_step(T* w, const T* g, int64_t n, double lr, double contrib, cudaStream_t st);
 template <typename T>

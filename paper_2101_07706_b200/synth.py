@@ -40,7 +40,10 @@ SHAPES = {
                      p_intra=0.50),
     # YouTube: 1.1M nodes, 6.1M CSR entries, 2048-d multi-hot, 64 labels
     "youtube": dict(n=1_100_000, m=3_050_000, F=2048, C=64, feat="bow", train=0.70, val=0.10,
-                    p_intra=0.50),
+                    p_intra=0.50, multilabel=0.03),
+    # reduced YouTube-like graph for the multi-label parity tests
+    "youtube_s": dict(n=30000, m=90000, F=256, C=64, feat="bow", train=0.70, val=0.10,
+                      p_intra=0.50, multilabel=0.03),
 }
 
 
@@ -139,7 +142,7 @@ def make_shaped_graph(name: str, seed: int = 0, device: str | None = None,
     s = SHAPES[name]
     n, m, F, C = s["n"], s["m"], s["F"], s["C"]
     root = np.random.SeedSequence([seed, int.from_bytes(name.encode()[:8].ljust(8, b"\0"), "little")])
-    r_edge, r_feat, r_mask = [np.random.default_rng(c) for c in root.spawn(3)]
+    r_edge, r_feat, r_mask, r_lab = [np.random.default_rng(c) for c in root.spawn(4)]
     blocks = _blocks(n, C)
     u, v = _edge_draws(n, m, blocks, C, s["p_intra"], r_edge)
     if device is not None and device != "cpu":
@@ -168,4 +171,8 @@ def make_shaped_graph(name: str, seed: int = 0, device: str | None = None,
     tr[order[:n_tr]] = True
     va[order[n_tr:n_tr + n_va]] = True
     te[order[n_tr + n_va:]] = True
-    return ShapedGraph(name, n, offs, col, w, x, blocks.copy(), tr, va, te, C)
+    labels = blocks.copy()
+    if s.get("multilabel"):  # multi-hot: the block's label plus independent extra labels
+        labels = r_lab.random((n, C), dtype=np.float32) < np.float32(s["multilabel"])
+        labels[np.arange(n), blocks % C] = True
+    return ShapedGraph(name, n, offs, col, w, x, labels, tr, va, te, C)

@@ -294,20 +294,25 @@ def forward(model: GcnModel, plan: SamplePlan, features: np.ndarray) -> np.ndarr
     return out.astype(np.float64)
 
 
-def loss_and_backward(model: GcnModel, plan: SamplePlan, features: np.ndarray, labels: np.ndarray):
+def loss_and_backward(model: GcnModel, plan: SamplePlan, features: np.ndarray, labels: np.ndarray,
+                      pos_weight: float = 50.0):
     """Mean softmax cross-entropy over labelled batch rows and all weight gradients
-    (training.py:272-318), computed on the GPU."""
+    (training.py:272-318), computed on the GPU.  With an n x C multi-hot ``labels`` matrix
+    the head is the multi-label BCE-with-logits (positive weight ``pos_weight``, mean over
+    batch rows x classes; extension for the YouTube-shaped config, no reference code)."""
     _check_plan(model, plan)
     torch = _torch()
     dtype = D.compute_dtype()
     lease = plan._lease
-    batch_labels = np.asarray(labels)[plan.batch]
-    if not np.any(batch_labels >= 0):
+    labels = np.asarray(labels)
+    multi = labels.ndim == 2
+    if not multi and not np.any(labels[plan.batch] >= 0):
         raise ValueError("batch contains no labeled nodes")
     lease.dg.ensure_features(features, dtype)
-    lease.dg.ensure_labels(np.asarray(labels))
+    lease.dg.ensure_labels(labels)
     dims = [features.shape[1]] + [w.shape[1] for w in model.weights]
     gcn = lease.ps.gcn(dims, dtype)
+    check(lib.skg_gcn_set_loss(gcn, 1 if multi else 0, float(pos_weight) if multi else 1.0))
     ws, wp = _device_weights(model.weights, dtype)
     gs = [torch.empty_like(w) for w in ws]
     gp = np.array([g.data_ptr() for g in gs], dtype=np.uint64)
@@ -350,11 +355,26 @@ class EvalResult:
     micro_f1: float
 
 
+def multilabel_scores(logits: np.ndarray, y: np.ndarray):
+    """(subset accuracy, micro-F1) of z > 0 against multi-hot targets."""
+    pred = logits > 0
+    truth = np.asarray(y) != 0
+    tp = float(np.sum(pred & truth))
+    fp = float(np.sum(pred & ~truth))
+    fn = float(np.sum(~pred & truth))
+    denom = 2 * tp + fp + fn
+    return float(np.mean(np.all(pred == truth, axis=1))), (2 * tp / denom if denom > 0 else 0.0)
+
+
 def evaluate(model: GcnModel, g: WeightedGraph, nodes) -> EvalResult:
-    """Argmax accuracy and micro-F1 (training.py:343-363)."""
+    """Argmax accuracy and micro-F1 (training.py:343-363); multi-hot labels: subset
+    accuracy and micro-F1 of z > 0."""
     nodes = node_set(nodes)
     if len(nodes) == 0:
         raise ValueError("empty evaluation node set")
+    if g.labels is not None and np.asarray(g.labels).ndim == 2:
+        acc, f1 = multilabel_scores(predict_logits(model, g)[nodes], np.asarray(g.labels)[nodes])
+        return EvalResult(accuracy=acc, micro_f1=f1)
     if g.labels is None or np.any(g.labels[nodes] < 0):
         raise ValueError("evaluation nodes must be labeled")
     preds = np.argmax(predict_logits(model, g)[nodes], axis=1)
@@ -470,10 +490,13 @@ class Trainer:
 
     def __init__(self, g, partition, model, cfg, *, batch_size, lr, mode, seed,
                  sampler="ladies", subgraph_size=None, optimizer="sgd", dtype=None,
-                 epochs=1, workers=None, ahead=1, shard_features=None, streams=1):
+                 epochs=1, workers=None, ahead=1, shard_features=None, streams=1,
+                 loss="auto", pos_weight=50.0):
         torch = _torch()
         if g.features is None or g.labels is None or g.train_mask is None:
             raise ValueError("training needs features, labels and masks")
+        if loss not in ("auto", "ce", "bce"):
+            raise ValueError(f"unknown loss {loss!r}")
         if sampler not in ("ladies", "saint"):
             raise ValueError(f"unknown sampler {sampler!r}")
         if sampler == "saint" and subgraph_size is None:
@@ -530,6 +553,11 @@ class Trainer:
                 _saint_set(self.dg, ps, self.all_train, mode != "local")
             self.bufs.append((ps, ps.gcn(self.dims, self.dtype)))
         self.ps, self.gcn = self.bufs[0]
+        # head: softmax CE for class labels, multi-label BCE for an n x C multi-hot matrix
+        self.multilabel = np.asarray(g.labels).ndim == 2 if loss == "auto" else loss == "bce"
+        for _, gcn in self.bufs:
+            check(lib.skg_gcn_set_loss(gcn, 1 if self.multilabel else 0,
+                                       float(pos_weight) if self.multilabel else 1.0))
         self._peer_ptrs = []
         if shard_features is None:
             shard_features = self.world > 1
@@ -773,7 +801,8 @@ class Trainer:
 def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, cfg: SamplerConfig, *,
                       epochs: int, batch_size: int, lr: float, mode: str, seed: int,
                       sampler: str = "ladies", subgraph_size: int | None = None,
-                      optimizer: str = "sgd", ahead: int = 4, streams: int = 2) -> tuple:
+                      optimizer: str = "sgd", ahead: int = 4, streams: int = 2,
+                      pos_weight: float = 50.0) -> tuple:
     """Data-parallel training with per-iteration gradient averaging (training.py:430-518).
 
     Single process: all workers run on this GPU.  Under torch.distributed (one process
@@ -784,7 +813,7 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
     torch = _torch()
     tr = Trainer(g, partition, model, cfg, batch_size=batch_size, lr=lr, mode=mode, seed=seed,
                  sampler=sampler, subgraph_size=subgraph_size, optimizer=optimizer, epochs=epochs,
-                 ahead=ahead, streams=streams)
+                 ahead=ahead, streams=streams, pos_weight=pos_weight)
     k, L = tr.k, tr.L
     metrics = Metrics()
     val_nodes = np.flatnonzero(g.val_mask) if g.val_mask is not None else np.empty(0, dtype=np.int64)
@@ -805,12 +834,21 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
             loss_sum, loss_cnt, ledger = reduce_epoch_stats(tr.dist, loss_sum, loss_cnt, ledger)
         ledger_np = ledger.cpu().numpy()
         logits = _predict_device(tr.dg, tr.wviews, tr.dims, tr.dtype)
-        preds = torch.argmax(logits, dim=1)
-        correct = (preds == labels_t).cpu().numpy()
-        val_acc = float(np.mean(correct[val_nodes])) if len(val_nodes) else 0.0
+        if tr.multilabel:  # accuracy columns carry micro-F1 of z > 0 for multi-hot labels
+            zl = logits.double().cpu().numpy()
+            ylab = np.asarray(g.labels)
+
+            def score(nodes):
+                return multilabel_scores(zl[nodes], ylab[nodes])[1] if len(nodes) else 0.0
+        else:
+            correct = (torch.argmax(logits, dim=1) == labels_t).cpu().numpy()
+
+            def score(nodes):
+                return float(np.mean(correct[nodes])) if len(nodes) else 0.0
+        val_acc = score(val_nodes)
         for w in range(k):
             tw = tr.worker_train[w]
-            train_acc = float(np.mean(correct[tw])) if len(tw) else 0.0
+            train_acc = score(tw)
             mean_loss = float(loss_sum[w] / loss_cnt[w]) if loss_cnt[w] else 0.0
             metrics.rows.append(MetricRow(epoch=epoch, worker=w, loss=mean_loss,
                                           train_acc=train_acc, val_acc=val_acc,
