@@ -216,11 +216,19 @@ def algorithmic_sampler_bytes(stats_rows, saint=False):
 def run_ours(args):
     import torch
     world, rank, local = dist_setup(args)
-    torch.cuda.set_device(local)
+    # one process per GPU; more ranks than GPUs (functional checks on a one-GPU box) share
+    # devices round-robin and must use SKG_DIST_BACKEND=gloo (NCCL needs distinct GPUs)
+    dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    local = dev
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("SKG_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     import paper_2101_07706_b200 as P
     from paper_2101_07706_b200._native import check, lib, ptr, MODES
 

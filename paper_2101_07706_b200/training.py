@@ -859,7 +859,10 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
         tr.run(pairs, on_iteration=end_of_epoch)
         tr.check_errors()
         tr.weights_to_model()
-        ledger_all = CommLedger(tr.ledger.cpu().numpy()[:epochs].copy())
+        led = tr.ledger.clone()
+        if tr.world > 1:  # each rank counted its own workers (training.py:117-134 is global)
+            tr.dist.all_reduce(led)
+        ledger_all = CommLedger(led.cpu().numpy()[:epochs].copy())
     finally:
         tr.close()
     return metrics, ledger_all
