@@ -1121,7 +1121,7 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
     }
     cv.add(g->G0lo, (size_t)S * R * g->ld_max * es);
   }
-  cv.add(g->parts, (size_t)S * wmax * es);
+  cv.add(g->parts, (size_t)S * kMaxKSplit * wmax * es);
   cv.add(g->row_loss, (size_t)S * R);
   cv.add(g->d_layers, (size_t)L * S);
   cv.add(g->d_slots, (size_t)S);
@@ -1304,10 +1304,12 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     P.stride = g->part_elems;
     P.ld = dn;
     bool done = false;
+    int ks = 1;  // K split inside each slot: partial (slot, run) blocks in slot-major order
     if constexpr (F32) {
       if (tc) {
+        ks = gemm_tc_ksplit(n, dl, dn, Ri);
         rc = gemm_tc(mode, true, false, n, dl, dn, Ri, nullptr, rows, op(g->U[l], g->Ulo[l], g->ld[l], g->ld[l]),
-                     op(g->G0, g->G0lo, g->ld_max, G.ld), P, false, st);
+                     op(g->G0, g->G0lo, g->ld_max, G.ld), P, false, st, ks);
         if (rc) return rc;
         done = true;
       }
@@ -1315,7 +1317,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     if (!done)
       gemm_simt<T>(true, false, n, dl, dn, Ri, nullptr, rows, act<T>(g->U[l], R, g->ld[l], g->ld[l], z0), G,
                    P, false, st);
-    reduce_slots<T>(P.base, P.stride, n, dl, dn, dn, reinterpret_cast<T*>(gp[l]), dn, accum, st);
+    reduce_slots<T>(P.base, P.stride, n * ks, dl, dn, dn, reinterpret_cast<T*>(gp[l]), dn, accum, st);
     if (l == 0) break;
     // G_u = G W_l^T ; G <- (Block_l^T G_u) * [H_l > 0]
     Gu.ld = g->ld[l];

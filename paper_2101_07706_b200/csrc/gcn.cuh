@@ -72,10 +72,16 @@ __device__ __forceinline__ float tf32_rna(float x) {
 }
 
 extern int g_gemm_mode;  // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
-// C_z = op(A_z) op(B_z) (+ C_z) on tcgen05 (TMA-fed); M (or K) per slot from dM / dK
+// C_z = op(A_z) op(B_z) (+ C_z) on tcgen05 (TMA-fed); M (or K) per slot from dM / dK.
+// ks > 1 splits every slot's K into ks contiguous runs of 32-wide chunks: output block
+// z * ks + j holds run j of slot z (partials for a fixed-order reduction).
+constexpr int kMaxKSplit = 4;
 int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
             const int32_t* const* dK, const TcOp& A, const TcOp& B, Act<float> C, bool acc,
-            cudaStream_t st);
+            cudaStream_t st, int ks = 1);
+// K split (1 .. kMaxKSplit) for an n-slot GEMM whose output is reduced afterwards: 1
+// unless forced (SKG_GEMM_KSPLIT / skg_debug_gemm_ksplit); see plan_bn in gemm_tc.cu
+int gemm_tc_ksplit(int n, int M, int N, int K);
 void split_tf32(const float* in, int64_t ld_in, int64_t rows, int64_t cols, float* hi, float* lo,
                 int64_t ld_out, cudaStream_t st);
 void split_weights(const WSplitTable& t, cudaStream_t st);

@@ -127,13 +127,24 @@ struct TcMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
 };
 
+// debug timeline of CTA (0, 0, 0) (globaltimer ns): [0] start, [1] after setup,
+// [2 + kc] stage kc full at the MMA warp, [34 + kc] TMA kc issued, [66] accumulator done
+// at the epilogue, [67] epilogue end (kc < 32); tools/gemm_trace.py
+__device__ unsigned long long g_tc_trace[68];
+__device__ int g_tc_trace_on;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // C_z = op(A_z) op(B_z) (+ C_z) on tensor cores; op(A) M x K, op(B) K x N.
 // TA: A stored K x M (contiguous along M); TB: B stored N x K (contiguous along K).
 template <bool TA, bool TB, int BN, int MODE>
 __global__ void __launch_bounds__(tc::NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ TcMaps maps, int Mfix, int N, int Kfix,
               const int32_t* const* dM, const int32_t* const* dK, int a_slots, int b_slots,
-              Act<float> C, int accumulate) {
+              Act<float> C, int accumulate, int ks) {
   SKG_PDL_PROLOGUE();
   using namespace tc;
   using CF = Cfg<BN, MODE>;
@@ -146,13 +157,18 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   __shared__ uint32_t tmem_base;
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
 
-  const int z = blockIdx.z;
+  const bool tr = g_tc_trace_on && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+  if (tr && threadIdx.x == 0) g_tc_trace[0] = gtimer();
+  const int zc = blockIdx.z;  // output block
+  const int z = zc / ks, kz = zc - z * ks;
   const int M = dM ? *dM[z] : Mfix;
   const int K = dK ? *dK[z] : Kfix;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   if (m0 >= M) return;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nk = K > 0 ? (K + BK - 1) / BK : 0;
+  const int nk_all = K > 0 ? (K + BK - 1) / BK : 0;
+  const int kc0 = (int)((long long)nk_all * kz / ks);  // this CTA's run of K chunks
+  const int nk = (int)((long long)nk_all * (kz + 1) / ks) - kc0;
 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -172,6 +188,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;");
   const uint32_t tmem = tmem_base;
+  if (tr && threadIdx.x == 0) g_tc_trace[1] = gtimer();
 
   if (warp == 0) {
     // ---------------- TMA producer
@@ -182,7 +199,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
         if (kc >= STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((kc / STAGES) - 1) & 1));
         uint8_t* st = smem + s * CF::STAGE;
         mbar_expect_tx(&full_bar[s], (uint32_t)CF::STAGE);
-        const int k0 = kc * BK;
+        if (tr && kc < 32) g_tc_trace[34 + kc] = gtimer();
+        const int k0 = (kc0 + kc) * BK;
 #pragma unroll
         for (int part = 0; part < CF::PARTS; ++part) {
           uint8_t* sa = st + part * (CF::A_BYTES + CF::B_BYTES);
@@ -218,6 +236,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
       for (int kc = 0; kc < nk; ++kc) {
         const int s = kc % STAGES;
         mbar_wait(&full_bar[s], (uint32_t)((kc / STAGES) & 1));
+        if (tr && kc < 32) g_tc_trace[2 + kc] = gtimer();
         asm volatile("tcgen05.fence::after_thread_sync;");
         uint8_t* st = smem + s * CF::STAGE;
         const uint32_t a_hi = smem_u32(st), b_hi = a_hi + CF::A_BYTES;
@@ -240,11 +259,12 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   } else {
     // ---------------- epilogue: TMEM lane quarter (warp % 4), all BN columns
     mbar_wait(&done_bar, 0u);
+    if (tr && threadIdx.x == 64) g_tc_trace[66] = gtimer();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int lg = warp & 3;
     const int row = m0 + lg * 32 + lane;
     const uint32_t taddr_row = tmem + ((uint32_t)(lg * 32) << 16);
-    float* __restrict__ c = C.at(z);
+    float* __restrict__ c = C.at(zc);
     const bool vecC = (C.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
     const bool empty_k = nk == 0;  // no MMA ran: the product is zero
 #pragma unroll 1
@@ -284,6 +304,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+  if (tr && threadIdx.x == 64) g_tc_trace[67] = gtimer();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
@@ -399,7 +420,7 @@ int op_maps(const TcOp& op, bool mn, int64_t mn_extent, int64_t k_extent, int ro
 
 template <bool TA, bool TB, int BN, int MODE>
 static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
-                     const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st) {
+                     const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st, int ks) {
   using CF = tc::Cfg<BN, MODE>;
   TcMaps maps;
   // A: M x K (TA: stored K x M); B: K x N (TB: stored N x K)
@@ -413,39 +434,72 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
     attr = true;
   }
-  dim3 grid((N + BN - 1) / BN, (M + tc::BM - 1) / tc::BM, n);
+  dim3 grid((N + BN - 1) / BN, (M + tc::BM - 1) / tc::BM, n * ks);
   const int as = A.stride ? n : 1, bs = B.stride ? n : 1;
-  launch_k("k_gemm_tc", st, dim3(grid), dim3(tc::NTHREADS), CF::SMEM, kern, maps, M, N, K, dM, dK, as, bs, C, acc ? 1 : 0);
+  launch_k("k_gemm_tc", st, dim3(grid), dim3(tc::NTHREADS), CF::SMEM, kern, maps, M, N, K, dM, dK, as, bs, C,
+           acc ? 1 : 0, ks);
   return SKG_OK;
 }
 
-int g_bn_override = 0;  // debug / tuning: force the N tile (32, 64, 128, 256)
+int g_bn_override = 0;      // debug / tuning: force the N tile (32, 64, 128, 256)
+int g_ksplit_override = 0;  // debug / tuning: force the K split of split-K callers
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// N tile.  The 3xTF32 main loop is bound by shared-memory bandwidth (tools/gemm_trace.py:
+// one 128 x 64 x 32 stage per ~0.5 us = TMA write 48 KB + MMA operand reads 72 KB at
+// ~128 B/clk), and a CTA holds its SM (~200 KB of stages) for its whole life, with ~2 us of
+// fixed setup / first-load / epilogue time.  Inside the training step the GEMMs share the
+// GPU with the sampler streams, so total SM time counts, not one GEMM's latency: measured
+// on the Reddit-shaped step, BN = 128 everywhere gives 1358 it/s vs 1323 (BN = 64) and 1234
+// (BN = 256: a 2-stage ring, and mostly padding on the 41-class layer); splitting K inside
+// a slot (more, shorter CTAs) costs 1.5 %.  BN = 256 is kept for the wide (N >= 512)
+// multi-wave GraphSAINT GEMMs, where it halved their time.
+static int plan_bn(int n, int M, int N) {
+  if (N <= 32) return 32;
+  if (N <= 64) return 64;
+  const long long tiles256 = (long long)((M + tc::BM - 1) / tc::BM) * ((N + 255) / 256) * std::max(n, 1);
+  if (N >= 512 && tiles256 >= sm_count()) return 256;
+  return 128;
+}
+
+int gemm_tc_ksplit(int, int, int, int) {
+  static const int env = getenv("SKG_GEMM_KSPLIT") ? atoi(getenv("SKG_GEMM_KSPLIT")) : 0;
+  const int force = g_ksplit_override ? g_ksplit_override : env;
+  return force ? std::max(1, std::min(force, kMaxKSplit)) : 1;
+}
 
 template <bool TA, bool TB, int MODE>
 static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dM2,
-                       const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st) {
+                       const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st, int ks) {
   const int32_t* const* dK = dM2;
-  int bn = g_bn_override;
-  if (!bn) {
-    // 64-wide N tiles put 4x more CTAs on the skinny LADIES problems (M = a few thousand
-    // rows, one wave); once the grid spans several waves, wider tiles amortise the A reads
-    const long long tiles64 = (long long)((M + 127) / 128) * ((N + 63) / 64) * n;
-    bn = N <= 32 ? 32 : (tiles64 > 4 * 148 && N >= 256) ? 256 : (tiles64 > 2 * 148 && N >= 128) ? 128 : 64;
-  }
-  if (bn == 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
-  if (bn == 128) return launch_tc<TA, TB, 128, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
-  if (bn == 256) return launch_tc<TA, TB, 256, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
-  return launch_tc<TA, TB, 64, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st);
+  static const int env_bn = getenv("SKG_GEMM_BN") ? atoi(getenv("SKG_GEMM_BN")) : 0;
+  const int force = g_bn_override ? g_bn_override : env_bn;
+  const int bn = force ? force : plan_bn(n, M, N);
+  if (bn == 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
+  if (bn == 128) return launch_tc<TA, TB, 128, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
+  if (bn == 256) return launch_tc<TA, TB, 256, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
+  return launch_tc<TA, TB, 64, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
 }
 
 int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
             const int32_t* const* dK, const TcOp& A, const TcOp& B, Act<float> C, bool acc,
-            cudaStream_t st) {
+            cudaStream_t st, int ks) {
   if (M <= 0 || N <= 0 || n <= 0) return SKG_OK;
+  ks = std::max(1, std::min(ks, kMaxKSplit));
 #define TC_CASE(TA_, TB_)                                                                        \
   if (ta == TA_ && tb == TB_)                                                                    \
-    return mode == 3 ? dispatch_bn<TA_, TB_, 3>(n, M, N, K, dM, dK, A, B, C, acc, st)            \
-                     : dispatch_bn<TA_, TB_, 1>(n, M, N, K, dM, dK, A, B, C, acc, st);
+    return mode == 3 ? dispatch_bn<TA_, TB_, 3>(n, M, N, K, dM, dK, A, B, C, acc, st, ks)        \
+                     : dispatch_bn<TA_, TB_, 1>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
   TC_CASE(false, false)
   TC_CASE(true, false)
   TC_CASE(false, true)
@@ -560,6 +614,22 @@ extern "C" int skg_debug_gemm(int mode, int ta, int tb, int M, int N, int K, con
 // debug: time `iters` GEMMs on device-resident (zero) split operands, M x K by K x N
 extern "C" int skg_debug_gemm_bn(int bn) {
   skg::g_bn_override = bn;
+  return 0;
+}
+
+// debug / tuning: force the per-slot K split of the dW GEMMs (0 = planned)
+extern "C" int skg_debug_gemm_ksplit(int ks) {
+  skg::g_ksplit_override = ks;
+  return 0;
+}
+
+// debug: timeline of the next GEMMs' CTA (0, 0, 0); on = 1 arms, out (68 entries) reads
+extern "C" int skg_debug_tc_trace(int on, unsigned long long* out) {
+  cudaMemcpyToSymbol(skg::g_tc_trace_on, &on, sizeof(int));
+  if (out) {
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out, skg::g_tc_trace, sizeof(unsigned long long) * 68);
+  }
   return 0;
 }
 

@@ -8,6 +8,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <utility>
 
 namespace skg {
@@ -16,10 +18,15 @@ extern int g_pdl;
 bool prof_match(const char* name);
 void prof_record(cudaStream_t st, bool before);
 
+inline bool launch_debug() {
+  static const int on = getenv("SKG_LAUNCH_DEBUG") ? 1 : 0;
+  return on != 0;
+}
+
 // kernels of the GCN chain (main stream)
 inline bool gcn_kernel(const char* n) {
   static const char* const names[] = {"k_gemm_tc", "k_gemm_b", "k_gather_b", "k_spmm_b", "k_softmax_ce_b",
-                                      "k_loss_mean", "k_reduce_slots", "k_sgd", "k_adam", "k_split_weights",
+                                      "k_loss_mean", "k_reduce_slots", "k_sgd", "k_adam", "k_pad_weights",
                                       "k_ledger_add", "k_zero"};
   for (const char* m : names) {
     const char* a = n;
@@ -45,7 +52,10 @@ inline void launch_k(const char* name, cudaStream_t st, dim3 grid, dim3 block, s
   at[0].val.programmaticStreamSerializationAllowed = g_pdl == 1 || (g_pdl == 2 && gcn_kernel(name));
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+  const cudaError_t le = cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+  if (le != cudaSuccess && launch_debug())
+    fprintf(stderr, "skg: launch of %s (grid %u,%u,%u block %u smem %zu) failed: %s\n", name, grid.x, grid.y,
+            grid.z, block.x, smem, cudaGetErrorString(le));
   if (pm) prof_record(st, false);
   ++g_kernel_launches;
 }

@@ -108,6 +108,34 @@ def test_forward_backward_golden(case, dtype, rtol, atol):
         np.testing.assert_allclose(gr, ref, rtol=rtol, atol=scale(ref))
 
 
+@pytest.mark.parametrize("ks", [2, 3, 4])
+@pytest.mark.parametrize("case", G.cases("fb"))
+def test_forward_backward_dw_ksplit(case, ks):
+    """dW GEMMs with every slot's K split into ks runs (empty runs included for short
+    slots), reduced in (slot, run) order: same gradients as the golden run."""
+    from paper_2101_07706_b200._native import lib
+    pkg = P()
+    m = G.meta[case]
+    g = pkg_small_graph(m["graph"])
+    plan = pkg.ladies_plan(g, pkg_partition(m, g.n_nodes), m["worker"],
+                           np.array(m["batch"], dtype=np.int64), pkg_cfg(m), m["n_layers"],
+                           make_rng(m["rng"]))
+    x, y = G.get(case, "features"), G.get(case, "labels")
+    model = pkg.init_model(m["dims"], m["model_seed"])
+    old = pkg.compute_dtype()
+    pkg.set_compute_dtype("float32")
+    lib.skg_debug_gemm_ksplit(ks)
+    try:
+        loss, grads = pkg.loss_and_backward(model, plan, x, y)
+    finally:
+        lib.skg_debug_gemm_ksplit(0)
+        pkg.set_compute_dtype(old)
+    assert loss == pytest.approx(float(G.get(case, "loss")), rel=1e-4)
+    for l, gr in enumerate(grads):
+        ref = G.get(case, f"grad{l}")
+        np.testing.assert_allclose(gr, ref, rtol=1e-4, atol=1e-6 * max(1.0, float(np.abs(ref).max())))
+
+
 @pytest.mark.parametrize("case", G.cases("train"))
 def test_train_distributed_golden(case):
     pkg = P()
