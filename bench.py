@@ -433,7 +433,8 @@ def run_ours(args):
                                    "gcn_fwd_bwd_step": round(float(np.median(comp_ms)), 4)},
             "roofline": {"bound": top["bound"], "kernel": top["kernel"],
                          "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],
-                         "frac": top["frac"], "traffic": None,
+                         "frac": top["frac"], **ncu_traffic(top["kernel"]),
+                         **{k: top[k] for k in ("frac_of_3xtf32_peak", "peak_note") if k in top},
                          "per_launch": top["per_launch"], "avg_launch_us": top["avg_us"],
                          "share_of_step": round(top["total_ms"] / ms, 4),
                          "peak_source": "MEASURED_PEAKS.json"},
@@ -495,7 +496,10 @@ def kernel_table(lib, steps_resident, W, K, stats, tr, n_my, T, peaks):
             ach = per / avg_s / 1e12
             row = {"kernel": name + " (3xTF32 tcgen05; algorithmic flops, bf16 peak)",
                    "bound": "tensor", "unit": "TFLOP/s", "peak": tflops,
-                   "per_launch": {"flops": int(per)}}
+                   "per_launch": {"flops": int(per)},
+                   # each algorithmic flop is 3 TF32 MMA flops, TF32 runs at half the bf16 rate
+                   "frac_of_3xtf32_peak": round(ach / (tflops / 6.0), 5),
+                   "peak_note": "3xTF32 ceiling = measured bf16 / 2 (TF32 rate) / 3 (passes)"}
         else:
             per = models[name]
             ach = per / avg_s / 1e9
@@ -506,6 +510,24 @@ def kernel_table(lib, steps_resident, W, K, stats, tr, n_my, T, peaks):
                     "total_ms": round(tot.value, 4)})
         out.append(row)
     return out
+
+
+def ncu_traffic(kernel_label):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu --set full
+    extract (profiles/ncu_traffic.json, tools/ncu_traffic.py; cold-cache replay, so an upper
+    bound on the in-step traffic); null when the kernel was not captured."""
+    path = ROOT / "profiles" / "ncu_traffic.json"
+    base = kernel_label.split(" ")[0]
+    try:
+        table = json.loads(path.read_text())
+    except (OSError, ValueError):
+        return {"traffic": None}
+    hits = [k for k in table if k == base or k.startswith(base + "_")]
+    if not hits:
+        return {"traffic": None}
+    t = table[hits[0]]
+    return {"traffic": int(t["dram_bytes"]), "traffic_source": f"profiles/ncu_traffic.json ({hits[0]}, "
+            f"mean of {t['launches']} ncu --set full launches, cold cache)"}
 
 
 # ---------------------------------------------------------------------------- CPU oracle
