@@ -305,7 +305,16 @@ def run_ours(args):
         ev0.record(stream)
         for sd in tr.sides:  # the sampler streams start inside the timed region
             sd.wait_event(ev0)
-        steps_resident(W, K)
+        h0 = time.perf_counter()
+        if os.environ.get("SKG_BENCH_PROFILE"):  # host-side profile of the timed loop
+            import cProfile
+            import pstats
+            prof = cProfile.Profile()
+            prof.runcall(steps_resident, W, K)
+            pstats.Stats(prof, stream=sys.stderr).sort_stats("tottime").print_stats(25)
+        else:
+            steps_resident(W, K)
+        host_ms = (time.perf_counter() - h0) * 1e3  # enqueue time (the loop never syncs)
         ev1.record(stream)
         barrier()
     launches = P.kernel_launches() - launches0
@@ -429,6 +438,7 @@ def run_ours(args):
             "input_layer_remote_rows_per_iter": s0_remote,
             "sampled_nodes_per_s": round(sampled_nodes / (ms_per_step * 1e-3), 1),
             "gpu_launches": int(launches),
+            "host_enqueue_ms_per_step": round(host_ms / K, 4),
             "stages_ms_per_iter": {"sample": round(samp / T, 4),
                                    "gcn_fwd_bwd_step": round(float(np.median(comp_ms)), 4)},
             "roofline": {"bound": top["bound"], "kernel": top["kernel"],

@@ -7,6 +7,7 @@
 #include <mutex>
 #include <numeric>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/skewgcn_b200.h"
@@ -79,6 +80,7 @@ struct skg_ctx {
   int32_t* d_node_rank = nullptr;
   int32_t* d_node_row = nullptr;
   std::vector<void*> shards_owned;
+  uint64_t gen = 0;  // bumped by every setter: captured GCN graphs bake these pointers in
   GraphDev gdev() const {
     GraphDev g;
     g.n = n;
@@ -137,6 +139,16 @@ struct skg_plans {
 
 struct skg_gcn {
   skg_plans* ps = nullptr;
+  // CUDA graphs of the batched training step (gcn_dispatch), keyed by everything the
+  // captured launches bake in; losses land in loss_scratch and are copied out per call
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    unsigned long long launches;
+  };
+  std::unordered_map<std::string, GraphEntry> graphs;
+  cudaStream_t cap_stream = nullptr;
+  double* loss_scratch = nullptr;
+  std::vector<const int32_t*> batch_seen;  // batch pointer last written per slot descriptor
   int L = 0, dtype = DT_F32;
   std::vector<int64_t> dims, ld;
   int64_t ld_max = 0, R = 0;
@@ -398,6 +410,7 @@ extern "C" int skg_ctx_destroy(skg_ctx* c) {
 
 extern "C" int skg_ctx_set_features(skg_ctx* c, int dtype, int64_t dim, int64_t n_rows,
                                     const void* host_rows) {
+  if (c) ++c->gen;
   ARG(c && (dtype == DT_F32 || dtype == DT_F64) && dim > 0 && n_rows >= 0, "bad feature arguments");
   CK(cudaSetDevice(c->device));
   const size_t es = dtype == DT_F32 ? 4 : 8;
@@ -426,6 +439,7 @@ extern "C" int skg_ctx_set_features(skg_ctx* c, int dtype, int64_t dim, int64_t 
 
 extern "C" int skg_ctx_set_feature_map(skg_ctx* c, int n_ranks, const uint64_t* shard_ptrs,
                                        const int32_t* node_rank, const int32_t* node_row) {
+  if (c) ++c->gen;
   ARG(c && n_ranks >= 1 && shard_ptrs && node_rank && node_row, "bad feature map");
   CK(cudaSetDevice(c->device));
   cudaFree(c->d_shards);
@@ -464,6 +478,7 @@ extern "C" int skg_ctx_feature_ptr(skg_ctx* c, uint64_t* out_ptr, int64_t* out_l
 }
 
 extern "C" int skg_ctx_set_labels(skg_ctx* c, const int64_t* labels) {
+  if (c) ++c->gen;
   ARG(c && labels, "bad labels");
   CK(cudaSetDevice(c->device));
   std::vector<int32_t> l32(c->n);
@@ -476,6 +491,7 @@ extern "C" int skg_ctx_set_labels(skg_ctx* c, const int64_t* labels) {
 
 // multi-hot targets for the multi-label (BCE) loss: n x words uint64, bit k of word k/64
 extern "C" int skg_ctx_set_multilabels(skg_ctx* c, const uint64_t* words, int32_t n_classes) {
+  if (c) ++c->gen;
   ARG(c && words && n_classes >= 1, "bad multi-labels");
   CK(cudaSetDevice(c->device));
   const int32_t nw = (n_classes + 63) / 64;
@@ -488,6 +504,7 @@ extern "C" int skg_ctx_set_multilabels(skg_ctx* c, const uint64_t* words, int32_
 }
 
 extern "C" int skg_ctx_set_owner(skg_ctx* c, int32_t n_workers, const int32_t* owner) {
+  if (c) ++c->gen;
   ARG(c && owner && n_workers >= 1, "bad owner map");
   CK(cudaSetDevice(c->device));
   for (int64_t i = 0; i < c->n; ++i)
@@ -1176,6 +1193,9 @@ extern "C" int skg_gcn_set_loss(skg_gcn* g, int kind, double pos_weight) {
 
 extern "C" int skg_gcn_destroy(skg_gcn* g) {
   if (!g) return SKG_OK;
+  for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second.exec);
+  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+  if (g->loss_scratch) cudaFree(g->loss_scratch);
   cudaFree(g->arena);
   delete g;
   return SKG_OK;
@@ -1187,10 +1207,13 @@ namespace {
 int refresh_batches(skg_gcn* g, int z0, int n, cudaStream_t st) {
   skg_plans* ps = g->ps;
   if (ps->kind != KIND_LADIES) return SKG_OK;
+  if ((int)g->batch_seen.size() != g->n_slots) g->batch_seen.assign(g->n_slots, nullptr);
   for (int z = z0; z < z0 + n; ++z) {
     const int32_t* b = ps->h[z].batch;
+    if (b == g->batch_seen[z]) continue;  // unchanged since the last write
     CK(cudaMemcpyAsync(reinterpret_cast<char*>(g->d_slots + z) + offsetof(SlotDesc, batch), &b,
                        sizeof(b), cudaMemcpyHostToDevice, st));
+    g->batch_seen[z] = b;
   }
   return SKG_OK;
 }
@@ -1212,8 +1235,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
   const int L = g->L, S = g->n_slots;
   const int64_t R = g->R;
   const int Ri = (int)R;
-  int rc = refresh_batches(g, z0, n, st);
-  if (rc) return rc;
+  int rc = SKG_OK;
   // fp32 GEMMs on tcgen05 (mode 1 / 3) read TF32-split operands; 3xTF32 also needs lo parts
   constexpr bool F32 = sizeof(T) == 4;
   const int mode = F32 ? g_gemm_mode : 0;
@@ -1340,11 +1362,76 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
   return SKG_OK;
 }
 
+int gcn_eager(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, bool acc,
+              double* loss, bool backward, cudaStream_t st) {
+  return g->dtype == DT_F32 ? gcn_run<float>(g, z0, n, wp, gp, acc, loss, backward, st)
+                            : gcn_run<double>(g, z0, n, wp, gp, acc, loss, backward, st);
+}
+
+bool gcn_graphs_on() {
+  static const int on = getenv("SKG_GCN_GRAPH") ? atoi(getenv("SKG_GCN_GRAPH")) : 1;
+  return on != 0;
+}
+
+// Everything a captured step bakes into its launches: slots, weight / gradient buffers,
+// flags, loss head, GEMM configuration and the context's data pointers (generation).
+std::string graph_key(const skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, bool acc) {
+  std::string k;
+  auto put = [&](const void* p, size_t b) { k.append(reinterpret_cast<const char*>(p), b); };
+  const int hdr[7] = {z0, n, acc ? 1 : 0, g->loss_kind, g_gemm_mode, g_bn_override, g_ksplit_override};
+  put(hdr, sizeof(hdr));
+  put(&g->pos_weight, sizeof(double));
+  put(&g->ps->ctx->gen, sizeof(uint64_t));
+  put(wp, sizeof(uint64_t) * g->L);
+  put(gp, sizeof(uint64_t) * g->L);
+  return k;
+}
+
 int gcn_dispatch(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, bool acc,
                  double* loss, bool backward, cudaStream_t st) {
-  int rc = g->dtype == DT_F32 ? gcn_run<float>(g, z0, n, wp, gp, acc, loss, backward, st)
-                              : gcn_run<double>(g, z0, n, wp, gp, acc, loss, backward, st);
+  int rc = refresh_batches(g, z0, n, st);
   if (rc) return rc;
+  if (backward && loss && gp && gcn_graphs_on() && g_prof_target.empty()) {
+    // training step: replay a CUDA graph of the ~45 launches (host launch cost dominated)
+    const std::string key = graph_key(g, z0, n, wp, gp, acc);
+    auto it = g->graphs.find(key);
+    if (it == g->graphs.end()) {
+      if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
+      if (!g->loss_scratch) CK(cudaMalloc(&g->loss_scratch, sizeof(double) * std::max(g->n_slots, 1)));
+      const unsigned long long l0 = g_kernel_launches;
+      CK(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
+      rc = gcn_eager(g, z0, n, wp, gp, acc, g->loss_scratch, true, g->cap_stream);
+      cudaGraph_t graph = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(g->cap_stream, &graph);
+      const unsigned long long nl = g_kernel_launches - l0;
+      g_kernel_launches = l0;  // capturing launched nothing
+      if (rc || ce != cudaSuccess || !graph) {
+        if (graph) cudaGraphDestroy(graph);
+        cudaGetLastError();
+        if (rc) return rc;
+        set_error(std::string("gcn graph capture: ") + cudaGetErrorString(ce));
+        return SKG_ERR_CUDA;
+      }
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) {
+        set_error(std::string("gcn graph instantiate: ") + cudaGetErrorString(ie));
+        return SKG_ERR_CUDA;
+      }
+      if (g->graphs.size() > 256) {  // bound the cache (e.g. many weight buffers)
+        for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second.exec);
+        g->graphs.clear();
+      }
+      it = g->graphs.emplace(key, skg_gcn::GraphEntry{exec, nl}).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, st));
+    g_kernel_launches += it->second.launches;
+    CK(cudaMemcpyAsync(loss, g->loss_scratch, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  } else {
+    rc = gcn_eager(g, z0, n, wp, gp, acc, loss, backward, st);
+    if (rc) return rc;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("gcn: ") + cudaGetErrorString(e));

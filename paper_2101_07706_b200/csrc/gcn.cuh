@@ -71,7 +71,9 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float(r);
 }
 
-extern int g_gemm_mode;  // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
+extern int g_gemm_mode;        // fp32 GEMMs: 0 SIMT, 1 1xTF32 tcgen05, 3 3xTF32 tcgen05
+extern int g_bn_override;      // debug / tuning overrides of the GEMM tile plan
+extern int g_ksplit_override;
 // C_z = op(A_z) op(B_z) (+ C_z) on tcgen05 (TMA-fed); M (or K) per slot from dM / dK.
 // ks > 1 splits every slot's K into ks contiguous runs of 32-wide chunks: output block
 // z * ks + j holds run j of slot z (partials for a fixed-order reduction).
