@@ -21,6 +21,78 @@ static std::string g_prof_target;
 static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_pairs;
 static cudaEvent_t g_prof_open = nullptr;
 bool prof_match(const char* name) { return !g_prof_target.empty() && g_prof_target == name; }
+
+// CUDA graphs of fixed launch sequences (the training step, the LADIES sampler): the
+// per-call host cost of ~50-90 launches was the throughput limit.  A sequence is captured
+// once per key (everything its launches bake in) on a private stream and replayed with one
+// cudaGraphLaunch; per-call inputs live in device memory written before the replay.
+struct GraphEntry {
+  cudaGraphExec_t exec;
+  unsigned long long launches;  // kernels per replay (for the launch counter)
+};
+struct GraphCache {
+  std::unordered_map<std::string, GraphEntry> map;
+  cudaStream_t cap = nullptr;
+  ~GraphCache() { clear(); }
+  void clear() {
+    for (auto& kv : map) cudaGraphExecDestroy(kv.second.exec);
+    map.clear();
+  }
+};
+
+bool graphs_on() {
+  static const int on = getenv("SKG_GCN_GRAPH") ? atoi(getenv("SKG_GCN_GRAPH")) : 1;
+  return on != 0 && g_prof_target.empty();  // per-kernel profiling needs eager launches
+}
+
+template <typename Fn>
+int graph_run(GraphCache& gc, const std::string& key, cudaStream_t st, Fn&& launch) {
+  auto it = gc.map.find(key);
+  if (it == gc.map.end()) {
+    if (!gc.cap && cudaStreamCreateWithFlags(&gc.cap, cudaStreamNonBlocking) != cudaSuccess) {
+      set_error("graph capture stream");
+      return SKG_ERR_CUDA;
+    }
+    const unsigned long long l0 = g_kernel_launches;
+    if (cudaStreamBeginCapture(gc.cap, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("graph capture begin");
+      return SKG_ERR_CUDA;
+    }
+    int rc = launch(gc.cap);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(gc.cap, &graph);
+    const unsigned long long nl = g_kernel_launches - l0;
+    g_kernel_launches = l0;  // capturing launched nothing
+    if (rc || ce != cudaSuccess || !graph) {
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+      if (rc) return rc;
+      set_error(std::string("graph capture: ") + cudaGetErrorString(ce));
+      return SKG_ERR_CUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      set_error(std::string("graph instantiate: ") + cudaGetErrorString(ie));
+      return SKG_ERR_CUDA;
+    }
+    if (gc.map.size() >= 256) gc.clear();  // bound the cache
+    it = gc.map.emplace(key, GraphEntry{exec, nl}).first;
+  }
+  if (cudaGraphLaunch(it->second.exec, st) != cudaSuccess) {
+    set_error(std::string("graph launch: ") + cudaGetErrorString(cudaGetLastError()));
+    return SKG_ERR_CUDA;
+  }
+  g_kernel_launches += it->second.launches;
+  return SKG_OK;
+}
+
+template <typename T>
+void key_put(std::string& k, const T& v) {
+  k.append(reinterpret_cast<const char*>(&v), sizeof(T));
+}
 void prof_record(cudaStream_t st, bool before) {
   cudaEvent_t e;
   cudaEventCreate(&e);
@@ -135,18 +207,29 @@ struct skg_plans {
   std::vector<double*> d_local_norm;
   std::vector<int64_t> n_local;
   std::vector<bool> local_norm_ready;
+  GraphCache graphs;  // LADIES launch sequences per (plans, rows cap, context generation)
 };
+
+// the LADIES launch sequence for the first n slots (descriptors already on the device)
+int run_ladies(skg_plans* ps, int n, int max_upper, cudaStream_t st) {
+  skg_ctx* c = ps->ctx;
+  auto launch = [&](cudaStream_t s) {
+    return launch_ladies(c->gdev(), ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
+                         (int)ps->budget, s);
+  };
+  if (!graphs_on()) return launch(st);
+  std::string key;
+  key_put(key, n);
+  key_put(key, max_upper);
+  key_put(key, c->gen);
+  return graph_run(ps->graphs, key, st, launch);
+}
 
 struct skg_gcn {
   skg_plans* ps = nullptr;
-  // CUDA graphs of the batched training step (gcn_dispatch), keyed by everything the
-  // captured launches bake in; losses land in loss_scratch and are copied out per call
-  struct GraphEntry {
-    cudaGraphExec_t exec;
-    unsigned long long launches;
-  };
-  std::unordered_map<std::string, GraphEntry> graphs;
-  cudaStream_t cap_stream = nullptr;
+  // CUDA graphs of the batched training step (gcn_dispatch); losses land in loss_scratch
+  // and are copied to the caller's buffer after each replay
+  GraphCache graphs;
   double* loss_scratch = nullptr;
   std::vector<const int32_t*> batch_seen;  // batch pointer last written per slot descriptor
   int L = 0, dtype = DT_F32;
@@ -712,6 +795,8 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
 extern "C" int skg_plans_destroy(skg_plans* ps) {
   if (!ps) return SKG_OK;
   cudaSetDevice(ps->ctx->device);
+  ps->graphs.clear();
+  if (ps->graphs.cap) cudaStreamDestroy(ps->graphs.cap);
   cudaFree(ps->arena);
   cudaFree(ps->d_scal);
   cudaFree(ps->d_plans);
@@ -785,8 +870,7 @@ extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
   CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
   const int max_upper = ps->L > 1 ? std::max<int>(ps->cap_batch, (int)std::min<int64_t>(ps->budget, ps->cap_cand))
                                   : ps->cap_batch;
-  return launch_ladies(c->gdev(), ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
-                       (int)ps->budget, st);
+  return run_ladies(ps, n, max_upper, st);
 }
 
 extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* workers,
@@ -819,8 +903,7 @@ extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* wor
   CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
   const int max_upper = ps->L > 1 ? std::max<int>(ps->cap_batch, (int)std::min<int64_t>(ps->budget, ps->cap_cand))
                                   : ps->cap_batch;
-  return launch_ladies(c->gdev(), ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
-                       (int)ps->budget, st);
+  return run_ladies(ps, n, max_upper, st);
 }
 
 // column_norms(g, rows, candidates) (graph.py:198-220) by the pull formulation: for each
@@ -1193,8 +1276,8 @@ extern "C" int skg_gcn_set_loss(skg_gcn* g, int kind, double pos_weight) {
 
 extern "C" int skg_gcn_destroy(skg_gcn* g) {
   if (!g) return SKG_OK;
-  for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second.exec);
-  if (g->cap_stream) cudaStreamDestroy(g->cap_stream);
+  g->graphs.clear();
+  if (g->graphs.cap) cudaStreamDestroy(g->graphs.cap);
   if (g->loss_scratch) cudaFree(g->loss_scratch);
   cudaFree(g->arena);
   delete g;
@@ -1368,11 +1451,6 @@ int gcn_eager(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp,
                             : gcn_run<double>(g, z0, n, wp, gp, acc, loss, backward, st);
 }
 
-bool gcn_graphs_on() {
-  static const int on = getenv("SKG_GCN_GRAPH") ? atoi(getenv("SKG_GCN_GRAPH")) : 1;
-  return on != 0;
-}
-
 // Everything a captured step bakes into its launches: slots, weight / gradient buffers,
 // flags, loss head, GEMM configuration and the context's data pointers (generation).
 std::string graph_key(const skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, bool acc) {
@@ -1391,42 +1469,13 @@ int gcn_dispatch(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* 
                  double* loss, bool backward, cudaStream_t st) {
   int rc = refresh_batches(g, z0, n, st);
   if (rc) return rc;
-  if (backward && loss && gp && gcn_graphs_on() && g_prof_target.empty()) {
-    // training step: replay a CUDA graph of the ~45 launches (host launch cost dominated)
-    const std::string key = graph_key(g, z0, n, wp, gp, acc);
-    auto it = g->graphs.find(key);
-    if (it == g->graphs.end()) {
-      if (!g->cap_stream) CK(cudaStreamCreateWithFlags(&g->cap_stream, cudaStreamNonBlocking));
-      if (!g->loss_scratch) CK(cudaMalloc(&g->loss_scratch, sizeof(double) * std::max(g->n_slots, 1)));
-      const unsigned long long l0 = g_kernel_launches;
-      CK(cudaStreamBeginCapture(g->cap_stream, cudaStreamCaptureModeThreadLocal));
-      rc = gcn_eager(g, z0, n, wp, gp, acc, g->loss_scratch, true, g->cap_stream);
-      cudaGraph_t graph = nullptr;
-      const cudaError_t ce = cudaStreamEndCapture(g->cap_stream, &graph);
-      const unsigned long long nl = g_kernel_launches - l0;
-      g_kernel_launches = l0;  // capturing launched nothing
-      if (rc || ce != cudaSuccess || !graph) {
-        if (graph) cudaGraphDestroy(graph);
-        cudaGetLastError();
-        if (rc) return rc;
-        set_error(std::string("gcn graph capture: ") + cudaGetErrorString(ce));
-        return SKG_ERR_CUDA;
-      }
-      cudaGraphExec_t exec = nullptr;
-      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ie != cudaSuccess) {
-        set_error(std::string("gcn graph instantiate: ") + cudaGetErrorString(ie));
-        return SKG_ERR_CUDA;
-      }
-      if (g->graphs.size() > 256) {  // bound the cache (e.g. many weight buffers)
-        for (auto& kv : g->graphs) cudaGraphExecDestroy(kv.second.exec);
-        g->graphs.clear();
-      }
-      it = g->graphs.emplace(key, skg_gcn::GraphEntry{exec, nl}).first;
-    }
-    CK(cudaGraphLaunch(it->second.exec, st));
-    g_kernel_launches += it->second.launches;
+  if (backward && loss && gp && graphs_on()) {
+    // training step: replay a CUDA graph of its ~45 launches
+    if (!g->loss_scratch) CK(cudaMalloc(&g->loss_scratch, sizeof(double) * std::max(g->n_slots, 1)));
+    rc = graph_run(g->graphs, graph_key(g, z0, n, wp, gp, acc), st, [&](cudaStream_t cs) {
+      return gcn_eager(g, z0, n, wp, gp, acc, g->loss_scratch, true, cs);
+    });
+    if (rc) return rc;
     CK(cudaMemcpyAsync(loss, g->loss_scratch, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   } else {
     rc = gcn_eager(g, z0, n, wp, gp, acc, loss, backward, st);
