@@ -283,9 +283,13 @@ def run_ours(args):
         # plan arenas while the GCN consumes them in order on the main stream
         groups = [(g0, min(T, s0 + count - g0)) for g0 in range(s0, s0 + count, T)]
 
+        no_gcn = bool(os.environ.get("SKG_BENCH_SAMPLER_ONLY"))  # diagnostic: pipeline minus GCN
+
         def compute(g, b):
             g0, n = groups[g]
             for i in range(n):
+                if no_gcn:
+                    continue
                 tr.compute(0, (g0 + i) % per, i, b)
                 tr.reduce_and_step()
 
