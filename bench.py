@@ -379,28 +379,31 @@ def run_ours(args):
     h2d = [0]
 
     # each step's loss is copied to pinned host memory behind its GCN on the main stream and
-    # read by the host two steps later (no per-step stream drain); all are read in the region
-    ring = [torch.empty(n_my, dtype=torch.float64, pin_memory=True) for _ in range(4)]
-    ring_ev = [torch.cuda.Event() for _ in range(4)]
+    # read by the host LAG steps later (no per-step stream drain, and the host stays as far
+    # ahead as the sampler look-ahead: 2 groups of `ahead` steps); all are read in the region
+    LAG = max(2, 3 * T)
+    RING = LAG + 2
+    ring = [torch.empty(n_my, dtype=torch.float64, pin_memory=True) for _ in range(RING)]
+    ring_ev = [torch.cuda.Event() for _ in range(RING)]
     pending, host_losses = [], []
 
     def read_loss(e, it):
         h2d[0] += int(tr._boff[n_my]) * 4 + n_my * 32
         i = len(host_losses) + len(pending)
-        ring[i % 4].copy_(tr.losses[it % per], non_blocking=True)
-        ring_ev[i % 4].record(stream)
+        ring[i % RING].copy_(tr.losses[it % per], non_blocking=True)
+        ring_ev[i % RING].record(stream)
         pending.append(i)
-        while len(pending) > 2:
+        while len(pending) > LAG:
             j = pending.pop(0)
-            ring_ev[j % 4].synchronize()
-            host_losses.append(float(ring[j % 4].sum()))
+            ring_ev[j % RING].synchronize()
+            host_losses.append(float(ring[j % RING].sum()))
 
     pairs = [(s // per, s % per) for s in range(K)]
     t_e2e0 = time.perf_counter()
     tr.run(pairs, on_iteration=read_loss)
     for j in pending:
-        ring_ev[j % 4].synchronize()
-        host_losses.append(float(ring[j % 4].sum()))
+        ring_ev[j % RING].synchronize()
+        host_losses.append(float(ring[j % RING].sum()))
     barrier()
     assert len(host_losses) == K, "e2e: step losses not all read"
     e2e_ms = (time.perf_counter() - t_e2e0) * 1e3

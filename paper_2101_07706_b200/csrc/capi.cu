@@ -208,7 +208,38 @@ struct skg_plans {
   std::vector<int64_t> n_local;
   std::vector<bool> local_norm_ready;
   GraphCache graphs;  // LADIES launch sequences per (plans, rows cap, context generation)
+  // pinned staging of each sampling call's uploads (descriptors, batch ids); up_ev marks
+  // the last upload consumed by its stream before the host rewrites the staging
+  PlanDev* h_pin = nullptr;
+  int32_t* hb_pin = nullptr;
+  cudaEvent_t up_ev = nullptr;
+  bool up_armed = false;
 };
+
+// wait until the previous upload from the pinned staging has been consumed
+int staging_ready(skg_plans* ps) {
+  if (!ps->h_pin) {
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&ps->h_pin), sizeof(PlanDev) * std::max(ps->n_slots, 1),
+                     cudaHostAllocDefault));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&ps->hb_pin),
+                     sizeof(int32_t) * std::max<size_t>((size_t)ps->n_slots * ps->cap_batch, 1),
+                     cudaHostAllocDefault));
+    CK(cudaEventCreateWithFlags(&ps->up_ev, cudaEventDisableTiming));
+  }
+  if (ps->up_armed) CK(cudaEventSynchronize(ps->up_ev));
+  ps->up_armed = false;
+  return SKG_OK;
+}
+
+// descriptors of the first n slots (and nb batch ids, when given) -> device, async
+int upload_plans(skg_plans* ps, int n, size_t nb, cudaStream_t st) {
+  std::memcpy(ps->h_pin, ps->h.data(), sizeof(PlanDev) * n);
+  CK(cudaMemcpyAsync(ps->d_plans, ps->h_pin, sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
+  if (nb) CK(cudaMemcpyAsync(ps->d_batch, ps->hb_pin, sizeof(int32_t) * nb, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(ps->up_ev, st));
+  ps->up_armed = true;
+  return SKG_OK;
+}
 
 // the LADIES launch sequence for the first n slots (descriptors already on the device)
 int run_ladies(skg_plans* ps, int n, int max_upper, cudaStream_t st) {
@@ -797,6 +828,12 @@ extern "C" int skg_plans_destroy(skg_plans* ps) {
   cudaSetDevice(ps->ctx->device);
   ps->graphs.clear();
   if (ps->graphs.cap) cudaStreamDestroy(ps->graphs.cap);
+  if (ps->up_ev) {
+    cudaEventSynchronize(ps->up_ev);
+    cudaEventDestroy(ps->up_ev);
+  }
+  if (ps->h_pin) cudaFreeHost(ps->h_pin);
+  if (ps->hb_pin) cudaFreeHost(ps->hb_pin);
   cudaFree(ps->arena);
   cudaFree(ps->d_scal);
   cudaFree(ps->d_plans);
@@ -834,7 +871,9 @@ extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
   skg_ctx* c = ps->ctx;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
-  std::vector<int32_t> hb((size_t)n * ps->cap_batch);
+  int rc = staging_ready(ps);
+  if (rc) return rc;
+  int32_t* hb = ps->hb_pin;
   for (int i = 0; i < n; ++i) {
     int64_t len = batch_off[i + 1] - batch_off[i];
     if (len <= 0) {
@@ -865,8 +904,8 @@ extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
     P.batch = ps->d_batch + (size_t)i * ps->cap_batch;
     P.cand_norm = nullptr;
   }
-  CK(cudaMemcpyAsync(ps->d_batch, hb.data(), sizeof(int32_t) * hb.size(), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
+  rc = upload_plans(ps, n, (size_t)n * ps->cap_batch, st);
+  if (rc) return rc;
   CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
   const int max_upper = ps->L > 1 ? std::max<int>(ps->cap_batch, (int)std::min<int64_t>(ps->budget, ps->cap_cand))
                                   : ps->cap_batch;
@@ -882,6 +921,8 @@ extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* wor
   skg_ctx* c = ps->ctx;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  int rc = staging_ready(ps);
+  if (rc) return rc;
   for (int i = 0; i < n; ++i) {
     if (batch_len[i] <= 0) {
       set_error("empty batch");
@@ -899,7 +940,8 @@ extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* wor
     P.batch = reinterpret_cast<const int32_t*>(d_batch) + (size_t)i * batch_stride;
     P.cand_norm = nullptr;
   }
-  CK(cudaMemcpyAsync(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
+  rc = upload_plans(ps, n, 0, st);
+  if (rc) return rc;
   CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
   const int max_upper = ps->L > 1 ? std::max<int>(ps->cap_batch, (int)std::min<int64_t>(ps->budget, ps->cap_cand))
                                   : ps->cap_batch;
@@ -1066,7 +1108,12 @@ extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, in
       P.budget = std::min<int64_t>(ps->budget, ps->n_train);
     }
   }
-  CK(cudaMemcpyAsync(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
+  {
+    const int urc = staging_ready(ps);
+    if (urc) return urc;
+    const int prc = upload_plans(ps, n, 0, st);
+    if (prc) return prc;
+  }
   return launch_saint(c->gdev(), ps->d_plans, n, ps->cap_rows, ps->cap_cand, ps->cap_pairs,
                       (int)ps->budget, st);
 }
