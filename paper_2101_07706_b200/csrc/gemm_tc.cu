@@ -83,6 +83,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity));
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes));
 }
@@ -309,6 +313,206 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TCOLS));
 }
 
+// Persistent variant for multi-wave grids (GraphSAINT's 36K-row GEMMs): one CTA per SM
+// walks the tiles blockIdx.x, + gridDim.x, ... (N tile fastest, so consecutive tiles reuse
+// the A tile in L2).  The stage ring runs continuously across tiles (global chunk
+// counters carry the phases), and two TMEM accumulators alternate between the MMA warp
+// and the epilogue warps (acc_full / acc_empty), so a tile's epilogue and the next tile's
+// first loads overlap the main loop instead of idling the SM.
+template <bool TA, bool TB, int BN, int MODE>
+__global__ void __launch_bounds__(tc::NTHREADS, 1)
+    k_gemm_tc_p(const __grid_constant__ TcMaps maps, int Mfix, int N, int Kfix,
+                const int32_t* const* dM, const int32_t* const* dK, int a_slots, int b_slots,
+                Act<float> C, int accumulate, int ks, int n_tiles_n, int n_tiles_m, int n_tiles) {
+  SKG_PDL_PROLOGUE();
+  using namespace tc;
+  using CF = Cfg<BN, MODE>;
+  constexpr bool SPLIT = MODE == 3;
+  constexpr int STAGES = CF::STAGES;
+  constexpr int TCOLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  constexpr bool A_MN = TA, B_MN = !TB;
+  extern __shared__ uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full_bar[STAGES], empty_bar[STAGES], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base;
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_base)),
+                 "n"(2 * TCOLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);     // tcgen05.commit after a tile's last MMA
+      mbar_init(&acc_empty[b], 128);  // every epilogue thread, after its TMEM reads
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = tmem_base;
+
+  // tile -> (n0, m0, output block zc, slot z, K run); false when the tile is past the slot's M
+  auto tile_at = [&](int tile, int& n0, int& m0, int& zc, int& z, int& kc0, int& nk, int& M) {
+    const int nt = tile % n_tiles_n;
+    const int rest = tile / n_tiles_n;
+    const int mt = rest % n_tiles_m;
+    zc = rest / n_tiles_m;
+    z = zc / ks;
+    const int kz = zc - z * ks;
+    M = dM ? *dM[z] : Mfix;
+    const int K = dK ? *dK[z] : Kfix;
+    n0 = nt * BN;
+    m0 = mt * BM;
+    const int nk_all = K > 0 ? (K + BK - 1) / BK : 0;
+    kc0 = (int)((long long)nk_all * kz / ks);
+    nk = (int)((long long)nk_all * (kz + 1) / ks) - kc0;
+    return m0 < M;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      uint32_t it = 0;  // chunks issued by this CTA so far
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int n0, m0, zc, z, kc0, nk, M;
+        if (!tile_at(tile, n0, m0, zc, z, kc0, nk, M)) continue;
+        const int za = a_slots > 1 ? z : 0, zb = b_slots > 1 ? z : 0;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % STAGES;
+          if (it >= STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((it / STAGES) - 1) & 1));
+          uint8_t* st = smem + s * CF::STAGE;
+          mbar_expect_tx(&full_bar[s], (uint32_t)CF::STAGE);
+          const int k0 = (kc0 + kc) * BK;
+#pragma unroll
+          for (int part = 0; part < CF::PARTS; ++part) {
+            uint8_t* sa = st + part * (CF::A_BYTES + CF::B_BYTES);
+            uint8_t* sb = sa + CF::A_BYTES;
+            const CUtensorMap* ma = part ? &maps.a_lo : &maps.a_hi;
+            const CUtensorMap* mb = part ? &maps.b_lo : &maps.b_hi;
+            if (A_MN) {
+#pragma unroll
+              for (int i = 0; i < BM / 32; ++i) tma3(sa + i * 4096, ma, m0 + 32 * i, k0, za, &full_bar[s]);
+            } else {
+              tma3(sa, ma, k0, m0, za, &full_bar[s]);
+            }
+            if (B_MN) {
+#pragma unroll
+              for (int i = 0; i < BN / 32; ++i) tma3(sb + i * 4096, mb, n0 + 32 * i, k0, zb, &full_bar[s]);
+            } else {
+              tma3(sb, mb, k0, n0, zb, &full_bar[s]);
+            }
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = make_idesc(BM, BN, A_MN, B_MN);
+      constexpr uint32_t A_STEP = A_MN ? 1024 : 32, B_STEP = B_MN ? 1024 : 32;
+      constexpr uint32_t A_LBO = A_MN ? 4096 : 16, B_LBO = B_MN ? 4096 : 16;
+      constexpr uint32_t A_SBO = A_MN ? 512 : 1024, B_SBO = B_MN ? 512 : 1024;
+      constexpr uint32_t A_LAY = A_MN ? 1 : 2, B_LAY = B_MN ? 1 : 2;
+      uint32_t it = 0, lt = 0;  // chunks consumed, tiles computed by this CTA
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        int n0, m0, zc, z, kc0, nk, M;
+        if (!tile_at(tile, n0, m0, zc, z, kc0, nk, M)) continue;
+        const uint32_t b = lt & 1u, u = lt >> 1;
+        if (u >= 1) mbar_wait(&acc_empty[b], (u - 1) & 1u);  // the epilogue drained buffer b
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t acc = tmem + b * TCOLS;
+        for (int kc = 0; kc < nk; ++kc, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(&full_bar[s], (uint32_t)((it / STAGES) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          uint8_t* st = smem + s * CF::STAGE;
+          const uint32_t a_hi = smem_u32(st), b_hi = a_hi + CF::A_BYTES;
+          const uint32_t a_lo = b_hi + CF::B_BYTES, b_lo = a_lo + CF::A_BYTES;
+#pragma unroll
+          for (int k8 = 0; k8 < BK / 8; ++k8) {
+            const uint64_t ah = make_desc(a_hi + k8 * A_STEP, A_LBO, A_SBO, A_LAY);
+            const uint64_t bh = make_desc(b_hi + k8 * B_STEP, B_LBO, B_SBO, B_LAY);
+            mma_tf32(acc, ah, bh, idesc, (kc > 0 || k8 > 0) ? 1u : 0u);
+            if (SPLIT) {
+              mma_tf32(acc, ah, make_desc(b_lo + k8 * B_STEP, B_LBO, B_SBO, B_LAY), idesc, 1u);
+              mma_tf32(acc, make_desc(a_lo + k8 * A_STEP, A_LBO, A_SBO, A_LAY), bh, idesc, 1u);
+            }
+          }
+          mma_commit(&empty_bar[s]);
+        }
+        mma_commit(&acc_full[b]);  // arrives at once when nk == 0 (no MMA ran)
+        ++lt;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue: TMEM lane quarter (warp % 4) of the tile's accumulator
+    const int lg = warp & 3;
+    uint32_t lt = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      int n0, m0, zc, z, kc0, nk, M;
+      if (!tile_at(tile, n0, m0, zc, z, kc0, nk, M)) continue;
+      const uint32_t b = lt & 1u, u = lt >> 1;
+      mbar_wait(&acc_full[b], u & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int row = m0 + lg * 32 + lane;
+      const uint32_t taddr_row = tmem + b * TCOLS + ((uint32_t)(lg * 32) << 16);
+      float* __restrict__ c = C.at(zc);
+      const bool vecC = (C.ld % 4 == 0) && ((reinterpret_cast<uintptr_t>(c) & 15) == 0);
+      const bool empty_k = nk == 0;
+#pragma unroll 1
+      for (int cb = 0; cb < BN && n0 + cb < N; cb += 16) {
+        uint32_t v[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15])
+            : "r"(taddr_row + cb));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+        if (row < M) {
+          float* crow = c + (int64_t)row * C.ld;
+#pragma unroll
+          for (int j4 = 0; j4 < 16; j4 += 4) {
+            const int col = n0 + cb + j4;
+            float o[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o[e] = empty_k ? 0.f : __uint_as_float(v[j4 + e]);
+            if (vecC && col + 3 < N) {
+              float4* p4 = reinterpret_cast<float4*>(crow + col);
+              float4 r4 = make_float4(o[0], o[1], o[2], o[3]);
+              if (accumulate) {
+                const float4 cur = *p4;
+                r4.x += cur.x; r4.y += cur.y; r4.z += cur.z; r4.w += cur.w;
+              }
+              *p4 = r4;
+            } else {
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                if (col + e < N) crow[col + e] = accumulate ? crow[col + e] + o[e] : o[e];
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&acc_empty[b]);  // buffer b may take the next tile's accumulation
+      ++lt;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TCOLS));
+}
+
 // ------------------------------------------------------------------ tensor maps (cached)
 namespace {
 
@@ -418,32 +622,6 @@ int op_maps(const TcOp& op, bool mn, int64_t mn_extent, int64_t k_extent, int ro
 
 }  // namespace
 
-template <bool TA, bool TB, int BN, int MODE>
-static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
-                     const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st, int ks) {
-  using CF = tc::Cfg<BN, MODE>;
-  TcMaps maps;
-  // A: M x K (TA: stored K x M); B: K x N (TB: stored N x K)
-  int rc = op_maps(A, TA, M, K, tc::BM, n, MODE == 3, &maps.a_hi, &maps.a_lo);
-  if (rc) return rc;
-  rc = op_maps(B, !TB, N, K, BN, n, MODE == 3, &maps.b_hi, &maps.b_lo);
-  if (rc) return rc;
-  auto kern = k_gemm_tc<TA, TB, BN, MODE>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
-    attr = true;
-  }
-  dim3 grid((N + BN - 1) / BN, (M + tc::BM - 1) / tc::BM, n * ks);
-  const int as = A.stride ? n : 1, bs = B.stride ? n : 1;
-  launch_k("k_gemm_tc", st, dim3(grid), dim3(tc::NTHREADS), CF::SMEM, kern, maps, M, N, K, dM, dK, as, bs, C,
-           acc ? 1 : 0, ks);
-  return SKG_OK;
-}
-
-int g_bn_override = 0;      // debug / tuning: force the N tile (32, 64, 128, 256)
-int g_ksplit_override = 0;  // debug / tuning: force the K split of split-K callers
-
 static int sm_count() {
   static int n = 0;
   if (!n) {
@@ -454,6 +632,48 @@ static int sm_count() {
   }
   return n;
 }
+
+template <bool TA, bool TB, int BN, int MODE>
+static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const int32_t* const* dK,
+                     const TcOp& A, const TcOp& B, Act<float> C, bool acc, cudaStream_t st, int ks) {
+  using CF = tc::Cfg<BN, MODE>;
+  TcMaps maps;
+  // A: M x K (TA: stored K x M); B: K x N (TB: stored N x K)
+  int rc = op_maps(A, TA, M, K, tc::BM, n, MODE == 3, &maps.a_hi, &maps.a_lo);
+  if (rc) return rc;
+  rc = op_maps(B, !TB, N, K, BN, n, MODE == 3, &maps.b_hi, &maps.b_lo);
+  if (rc) return rc;
+  const int as = A.stride ? n : 1, bs = B.stride ? n : 1;
+  const int tn = (N + BN - 1) / BN, tm = (M + tc::BM - 1) / tc::BM;
+  const long long tiles = (long long)tn * tm * n * ks;
+  static const int persist = getenv("SKG_GEMM_PERSIST") ? atoi(getenv("SKG_GEMM_PERSIST")) : 1;
+  if (persist && tiles > sm_count()) {
+    // multi-wave grid: persistent CTAs with double-buffered TMEM accumulators
+    auto pk = k_gemm_tc_p<TA, TB, BN, MODE>;
+    static bool pattr = false;
+    if (!pattr) {
+      cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+      pattr = true;
+    }
+    const int grid_p = (int)std::min<long long>(tiles, sm_count());
+    launch_k("k_gemm_tc", st, dim3(grid_p), dim3(tc::NTHREADS), CF::SMEM, pk, maps, M, N, K, dM, dK, as, bs, C,
+             acc ? 1 : 0, ks, tn, tm, (int)tiles);
+    return SKG_OK;
+  }
+  auto kern = k_gemm_tc<TA, TB, BN, MODE>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM);
+    attr = true;
+  }
+  dim3 grid(tn, tm, n * ks);
+  launch_k("k_gemm_tc", st, dim3(grid), dim3(tc::NTHREADS), CF::SMEM, kern, maps, M, N, K, dM, dK, as, bs, C,
+           acc ? 1 : 0, ks);
+  return SKG_OK;
+}
+
+int g_bn_override = 0;      // debug / tuning: force the N tile (32, 64, 128, 256)
+int g_ksplit_override = 0;  // debug / tuning: force the K split of split-K callers
 
 // N tile.  The 3xTF32 main loop is bound by shared-memory bandwidth (tools/gemm_trace.py:
 // one 128 x 64 x 32 stage per ~0.5 us = TMA write 48 KB + MMA operand reads 72 KB at

@@ -19,7 +19,10 @@ def _gemm(mode, ta, tb, A, B, M, N, K):
 
 
 SHAPES = [(512, 256, 602), (512, 41, 256), (602, 256, 512), (256, 41, 509), (130, 17, 33),
-          (1, 256, 8), (4096, 256, 256), (300, 300, 1)]
+          (1, 256, 8), (4096, 256, 256), (300, 300, 1),
+          # multi-wave grids -> persistent kernel (double-buffered TMEM accumulators), several
+          # tiles per CTA with partial M / N / K tiles; N tile 128 and 256
+          (20000, 300, 70), (9000, 512, 96), (37000, 520, 40)]
 
 
 @pytest.mark.parametrize("mode,tol", [(0, 1e-5), (1, 3e-3), (3, 1e-5)])
