@@ -692,10 +692,42 @@ static int plan_bn(int n, int M, int N) {
   return 128;
 }
 
-int gemm_tc_ksplit(int, int, int, int) {
+// Long contractions (>= 64 K chunks per slot, e.g. GraphSAINT's dW over 4500 subgraph
+// rows) with a grid under one wave: choose (BN, K split) jointly by the shared-memory
+// traffic model, waves x (chunks per tile + 2) x (128 + BN).  GraphSAINT dW (8 slots of
+// 512 x 512 x 4500): BN 256 with a 2-way split, one wave of 128 CTAs, instead of 128 CTAs
+// walking all 141 chunks.  Short contractions keep ks = 1 (measured faster in the LADIES step).
+constexpr int kLongK = 64 * tc::BK;
+struct LongKPlan {
+  int bn, ks;
+};
+static LongKPlan plan_long_k(int n, int M, int N, int K) {
+  const long long sms = sm_count();
+  const long long mt = (M + tc::BM - 1) / tc::BM;
+  const long long nk = (K + tc::BK - 1) / tc::BK;
+  LongKPlan best{128, 1};
+  double best_cost = 1e300;
+  for (int bn : {128, 256}) {
+    if (bn == 256 && N < 256) continue;
+    for (int ks = 1; ks <= kMaxKSplit; ++ks) {
+      const long long tiles = mt * ((N + bn - 1) / bn) * std::max(n, 1) * ks;
+      const long long waves = (tiles + sms - 1) / sms;
+      const double cost = (double)waves * ((nk + ks - 1) / ks + 2) * (128 + bn);
+      if (cost < best_cost * 0.97) {  // a split must win clearly (it adds a reduction)
+        best_cost = cost;
+        best = LongKPlan{bn, ks};
+      }
+    }
+  }
+  return best;
+}
+
+int gemm_tc_ksplit(int n, int M, int N, int K) {
   static const int env = getenv("SKG_GEMM_KSPLIT") ? atoi(getenv("SKG_GEMM_KSPLIT")) : 0;
   const int force = g_ksplit_override ? g_ksplit_override : env;
-  return force ? std::max(1, std::min(force, kMaxKSplit)) : 1;
+  if (force) return std::max(1, std::min(force, kMaxKSplit));
+  if (K >= kLongK && N > 64) return plan_long_k(n, M, N, K).ks;
+  return 1;
 }
 
 template <bool TA, bool TB, int MODE>
@@ -704,7 +736,7 @@ static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, con
   const int32_t* const* dK = dM2;
   static const int env_bn = getenv("SKG_GEMM_BN") ? atoi(getenv("SKG_GEMM_BN")) : 0;
   const int force = g_bn_override ? g_bn_override : env_bn;
-  const int bn = force ? force : plan_bn(n, M, N);
+  const int bn = force ? force : (K >= kLongK && N > 64) ? plan_long_k(n, M, N, K).bn : plan_bn(n, M, N);
   if (bn == 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
   if (bn == 128) return launch_tc<TA, TB, 128, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
   if (bn == 256) return launch_tc<TA, TB, 256, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);

@@ -22,7 +22,9 @@ SHAPES = [(512, 256, 602), (512, 41, 256), (602, 256, 512), (256, 41, 509), (130
           (1, 256, 8), (4096, 256, 256), (300, 300, 1),
           # multi-wave grids -> persistent kernel (double-buffered TMEM accumulators), several
           # tiles per CTA with partial M / N / K tiles; N tile 128 and 256
-          (20000, 300, 70), (9000, 512, 96), (37000, 520, 40)]
+          (20000, 300, 70), (9000, 512, 96), (37000, 520, 40),
+          # long contraction (141 K chunks: GraphSAINT's dW over a 4500-row subgraph)
+          (512, 512, 4500)]
 
 
 @pytest.mark.parametrize("mode,tol", [(0, 1e-5), (1, 3e-3), (3, 1e-5)])
