@@ -647,8 +647,11 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
   const int tn = (N + BN - 1) / BN, tm = (M + tc::BM - 1) / tc::BM;
   const long long tiles = (long long)tn * tm * n * ks;
   static const int persist = getenv("SKG_GEMM_PERSIST") ? atoi(getenv("SKG_GEMM_PERSIST")) : 1;
-  if (persist && tiles > sm_count()) {
-    // multi-wave grid: persistent CTAs with double-buffered TMEM accumulators
+  if (persist && tiles >= 3LL * sm_count()) {
+    // >= 3 waves (GraphSAINT's 36K-row GEMMs): persistent CTAs with double-buffered TMEM
+    // accumulators.  Not for shorter grids: persistent CTAs hold every SM until the GEMM
+    // ends, which starves the concurrent sampler streams (YouTube step: 1720 vs 1808 it/s
+    // when its 256-tile dW went persistent)
     auto pk = k_gemm_tc_p<TA, TB, BN, MODE>;
     static bool pattr = false;
     if (!pattr) {
@@ -701,7 +704,7 @@ constexpr int kLongK = 64 * tc::BK;
 struct LongKPlan {
   int bn, ks;
 };
-static LongKPlan plan_long_k(int n, int M, int N, int K) {
+static LongKPlan plan_long_k(int n, int M, int N, int K, int ks_fixed) {
   const long long sms = sm_count();
   const long long mt = (M + tc::BM - 1) / tc::BM;
   const long long nk = (K + tc::BK - 1) / tc::BK;
@@ -709,7 +712,8 @@ static LongKPlan plan_long_k(int n, int M, int N, int K) {
   double best_cost = 1e300;
   for (int bn : {128, 256}) {
     if (bn == 256 && N < 256) continue;
-    for (int ks = 1; ks <= kMaxKSplit; ++ks) {
+    const int ks_lo = ks_fixed > 0 ? ks_fixed : 1, ks_hi = ks_fixed > 0 ? ks_fixed : kMaxKSplit;
+    for (int ks = ks_lo; ks <= ks_hi; ++ks) {
       const long long tiles = mt * ((N + bn - 1) / bn) * std::max(n, 1) * ks;
       const long long waves = (tiles + sms - 1) / sms;
       const double cost = (double)waves * ((nk + ks - 1) / ks + 2) * (128 + bn);
@@ -726,7 +730,7 @@ int gemm_tc_ksplit(int n, int M, int N, int K) {
   static const int env = getenv("SKG_GEMM_KSPLIT") ? atoi(getenv("SKG_GEMM_KSPLIT")) : 0;
   const int force = g_ksplit_override ? g_ksplit_override : env;
   if (force) return std::max(1, std::min(force, kMaxKSplit));
-  if (K >= kLongK && N > 64) return plan_long_k(n, M, N, K).ks;
+  if (K >= kLongK && N > 64) return plan_long_k(n, M, N, K, 0).ks;
   return 1;
 }
 
@@ -736,7 +740,9 @@ static int dispatch_bn(int n, int M, int N, int K, const int32_t* const* dM, con
   const int32_t* const* dK = dM2;
   static const int env_bn = getenv("SKG_GEMM_BN") ? atoi(getenv("SKG_GEMM_BN")) : 0;
   const int force = g_bn_override ? g_bn_override : env_bn;
-  const int bn = force ? force : (K >= kLongK && N > 64) ? plan_long_k(n, M, N, K).bn : plan_bn(n, M, N);
+  // long contractions: the N tile for the K split actually used (1 for callers without
+  // partial outputs; a forward GEMM must not take the tile of a split plan)
+  const int bn = force ? force : (K >= kLongK && N > 64) ? plan_long_k(n, M, N, K, ks).bn : plan_bn(n, M, N);
   if (bn == 32) return launch_tc<TA, TB, 32, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
   if (bn == 128) return launch_tc<TA, TB, 128, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);
   if (bn == 256) return launch_tc<TA, TB, 256, MODE>(n, M, N, K, dM, dK, A, B, C, acc, st, ks);

@@ -20,9 +20,10 @@ def _gemm(mode, ta, tb, A, B, M, N, K):
 
 SHAPES = [(512, 256, 602), (512, 41, 256), (602, 256, 512), (256, 41, 509), (130, 17, 33),
           (1, 256, 8), (4096, 256, 256), (300, 300, 1),
-          # multi-wave grids -> persistent kernel (double-buffered TMEM accumulators), several
-          # tiles per CTA with partial M / N / K tiles; N tile 128 and 256
-          (20000, 300, 70), (9000, 512, 96), (37000, 520, 40),
+          # >= 3-wave grids -> persistent kernel (double-buffered TMEM accumulators), several
+          # tiles per CTA with partial M / N / K tiles (N tile 128 and 256); 9000 x 512 stays
+          # on the one-tile-per-CTA kernel (2 waves)
+          (60000, 300, 70), (9000, 512, 96), (37000, 520, 40),
           # long contraction (141 K chunks: GraphSAINT's dW over a 4500-row subgraph)
           (512, 512, 4500)]
 
