@@ -32,11 +32,13 @@ struct GraphEntry {
 };
 struct GraphCache {
   std::unordered_map<std::string, GraphEntry> map;
+  std::unordered_map<std::string, int> seen;  // keys run eagerly once (captured on reuse)
   cudaStream_t cap = nullptr;
   ~GraphCache() { clear(); }
   void clear() {
     for (auto& kv : map) cudaGraphExecDestroy(kv.second.exec);
     map.clear();
+    seen.clear();
   }
 };
 
@@ -49,6 +51,10 @@ template <typename Fn>
 int graph_run(GraphCache& gc, const std::string& key, cudaStream_t st, Fn&& launch) {
   auto it = gc.map.find(key);
   if (it == gc.map.end()) {
+    // a key's first use runs eagerly: one-off calls (e.g. loss_and_backward on freshly
+    // allocated weights) never pay a capture; the second use captures
+    if (gc.seen.size() > 4096) gc.seen.clear();
+    if (gc.seen[key]++ == 0) return launch(st);
     if (!gc.cap && cudaStreamCreateWithFlags(&gc.cap, cudaStreamNonBlocking) != cudaSuccess) {
       set_error("graph capture stream");
       return SKG_ERR_CUDA;
@@ -78,7 +84,10 @@ int graph_run(GraphCache& gc, const std::string& key, cudaStream_t st, Fn&& laun
       set_error(std::string("graph instantiate: ") + cudaGetErrorString(ie));
       return SKG_ERR_CUDA;
     }
-    if (gc.map.size() >= 256) gc.clear();  // bound the cache
+    if (gc.map.size() >= 256) {  // bound the cache
+      for (auto& kv : gc.map) cudaGraphExecDestroy(kv.second.exec);
+      gc.map.clear();
+    }
     it = gc.map.emplace(key, GraphEntry{exec, nl}).first;
   }
   if (cudaGraphLaunch(it->second.exec, st) != cudaSuccess) {
