@@ -139,16 +139,34 @@ __global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, T
       continue;
     }
     const int b = ip[r], e = ip[r + 1];
-    for (int64_t c = lane * 4; c < width; c += 128) {
-      Vec4<T> acc = Vec4<T>::zero();
+    // one pass over the row's nonzeros feeds up to NB 128-column blocks: NB gathers of
+    // every source row in flight per lane (each column still accumulates in nonzero order)
+    constexpr int NB = 2;
+    for (int64_t c0 = lane * 4; c0 < width; c0 += 128 * NB) {
+      Vec4<T> acc[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) acc[q] = Vec4<T>::zero();
+#pragma unroll 2
       for (int p = b; p < e; ++p) {
-        Vec4<T> x = Vec4<T>::load(a + (int64_t)ix[p] * A.ld + c);
-        if (RELU) x.relu();
-        acc.fma((T)vv[p], x);
+        const T s = (T)vv[p];
+        const T* src = a + (int64_t)ix[p] * A.ld;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+          if (c0 + 128 * q < width) {
+            Vec4<T> x = Vec4<T>::load(src + c0 + 128 * q);
+            if (RELU) x.relu();
+            acc[q].fma(s, x);
+          }
+        }
       }
-      if (TRANS) acc.mask(Vec4<T>::load(h + (int64_t)r * H.ld + c));
-      if (ol) store_split(acc, o + (int64_t)r * out.ld + c, ol + (int64_t)r * out.ld + c);
-      else acc.store(o + (int64_t)r * out.ld + c);
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int64_t c = c0 + 128 * q;
+        if (c >= width) continue;
+        if (TRANS) acc[q].mask(Vec4<T>::load(h + (int64_t)r * H.ld + c));
+        if (ol) store_split(acc[q], o + (int64_t)r * out.ld + c, ol + (int64_t)r * out.ld + c);
+        else acc[q].store(o + (int64_t)r * out.ld + c);
+      }
     }
   }
 }
