@@ -292,6 +292,7 @@ struct skg_gcn {
   double pos_weight = 1.0;
   int64_t part_elems = 0;
   double* row_loss = nullptr;
+  int32_t* nlab = nullptr;  // labelled rows per slot (softmax mean divisor)
   LayerDesc* d_layers = nullptr;      // [L][n_slots]
   SlotDesc* d_slots = nullptr;        // [n_slots]
   const int32_t** d_rows = nullptr;   // [L][n_slots] -> |S_{l+1}| scalars
@@ -1279,6 +1280,7 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   }
   cv.add(g->parts, (size_t)S * kMaxKSplit * wmax * es);
   cv.add(g->row_loss, (size_t)S * R);
+  cv.add(g->nlab, (size_t)S);
   cv.add(g->d_layers, (size_t)L * S);
   cv.add(g->d_slots, (size_t)S);
   cv.add(g->d_rows, (size_t)L * S);
@@ -1453,7 +1455,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
              (int)g->dims[L], g->pos_weight, G, G_lo, g->row_loss + (size_t)z0 * R, loss, st);
   } else {
     softmax_ce_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
-                    (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, loss, st);
+                    (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, loss, g->nlab + z0, st);
   }
   for (int l = L - 1; l >= 0; --l) {
     const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;

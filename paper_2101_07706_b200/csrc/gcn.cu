@@ -352,23 +352,31 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
 }
 
 // ------------------------------------------------------------------ softmax CE (K11)
+// labelled rows of every slot's batch, once per slot (the mean's divisor)
+__global__ void __launch_bounds__(1024) k_count_labels(const SlotDesc* sd, const int32_t* labels,
+                                                       int32_t* nlab) {
+  SKG_PDL_PROLOGUE();
+  const SlotDesc d = sd[blockIdx.x];
+  const int n = *d.n_batch;
+  typedef cub::BlockReduce<int, 1024> BR;
+  __shared__ typename BR::TempStorage tmp;
+  int cnt = 0;
+#pragma unroll 4
+  for (int r = threadIdx.x; r < n; r += blockDim.x) cnt += labels[d.batch[r]] >= 0;
+  const int tot = BR(tmp).Sum(cnt);
+  if (threadIdx.x == 0) nlab[blockIdx.x] = tot;
+}
+
 // training.py:293-308: per-row LSE loss and gradient (warp per row, all slots), then a
 // fixed-order per-slot mean.
 template <typename T>
 __global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T> Z, int C,
-                               Act<T> G, T* G_lo, int max_rows, double* row_loss, int64_t rl_stride) {
+                               Act<T> G, T* G_lo, int max_rows, double* row_loss, int64_t rl_stride,
+                               const int32_t* nlab_slot) {
   SKG_PDL_PROLOGUE();
   const SlotDesc d = sd[blockIdx.y];
   const int n = *d.n_batch;
-  __shared__ int s_nlab;
-  typedef cub::BlockReduce<int, 256> BR;
-  __shared__ typename BR::TempStorage tmp;
-  int cnt = 0;
-  for (int r = threadIdx.x; r < n; r += blockDim.x) cnt += labels[d.batch[r]] >= 0;
-  int tot = BR(tmp).Sum(cnt);
-  if (threadIdx.x == 0) s_nlab = tot;
-  __syncthreads();
-  const int nlab = s_nlab;
+  const int nlab = nlab_slot[blockIdx.y];  // labelled batch rows (k_count_labels)
   const T* z0 = Z.at(blockIdx.y);
   T* g0 = G.at(blockIdx.y);
   T* gl0 = G_lo ? G_lo + (int64_t)blockIdx.y * G.stride : nullptr;
@@ -417,27 +425,22 @@ __global__ void k_softmax_ce_b(const SlotDesc* sd, const int32_t* labels, Act<T>
   }
 }
 
-__global__ void k_loss_mean(const SlotDesc* sd, const int32_t* labels, const double* row_loss,
-                            int64_t rl_stride, double* loss_out) {
+__global__ void __launch_bounds__(1024) k_loss_mean(const SlotDesc* sd, const int32_t* labels,
+                                                    const double* row_loss, int64_t rl_stride,
+                                                    const int32_t* nlab, double* loss_out) {
   SKG_PDL_PROLOGUE();
   const SlotDesc d = sd[blockIdx.x];
   const int n = *d.n_batch;
-  typedef cub::BlockReduce<double, 256> BRD;
-  typedef cub::BlockReduce<int, 256> BRI;
+  typedef cub::BlockReduce<double, 1024> BRD;
   __shared__ typename BRD::TempStorage td;
-  __shared__ typename BRI::TempStorage ti;
   double s = 0.0;
-  int c = 0;
   const double* rl = row_loss + blockIdx.x * rl_stride;
-  for (int r = threadIdx.x; r < n; r += blockDim.x) {  // fixed assignment: deterministic
-    if (labels[d.batch[r]] >= 0) {
-      s += rl[r];
-      ++c;
-    }
-  }
-  double tot = BRD(td).Sum(s);
-  int cnt = BRI(ti).Sum(c);
+#pragma unroll 4
+  for (int r = threadIdx.x; r < n; r += blockDim.x)  // fixed assignment: deterministic
+    if (labels[d.batch[r]] >= 0) s += rl[r];
+  const double tot = BRD(td).Sum(s);
   if (threadIdx.x == 0) {
+    const int cnt = nlab[blockIdx.x];
     loss_out[blockIdx.x] = cnt ? tot / cnt : __longlong_as_double(0x7ff8000000000000LL);
     if (!cnt) atomicOr(d.err, EB_NO_LABELS);
   }
@@ -445,9 +448,11 @@ __global__ void k_loss_mean(const SlotDesc* sd, const int32_t* labels, const dou
 
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
-                  Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st) {
-  launch_k("k_softmax_ce_b", st, dim3(dim3(row_blocks(max_rows, n), n)), dim3(256), 0, k_softmax_ce_b<T>, sd, labels, Z, C, G, G_lo, max_rows, row_loss, max_rows);
-  launch_k("k_loss_mean", st, dim3(n), dim3(256), 0, k_loss_mean, sd, labels, row_loss, max_rows, loss_out);
+                  Act<T> G, T* G_lo, double* row_loss, double* loss_out, int32_t* nlab, cudaStream_t st) {
+  launch_k("k_count_labels", st, dim3(n), dim3(1024), 0, k_count_labels, sd, labels, nlab);
+  launch_k("k_softmax_ce_b", st, dim3(dim3(row_blocks(max_rows, n), n)), dim3(256), 0, k_softmax_ce_b<T>, sd, labels, Z, C, G, G_lo, max_rows, row_loss, max_rows, (const int32_t*)nlab);
+  launch_k("k_loss_mean", st, dim3(n), dim3(1024), 0, k_loss_mean, sd, labels, row_loss, (int64_t)max_rows,
+           (const int32_t*)nlab, loss_out);
 }
 
 // ------------------------------------------------------------------ multi-label BCE
@@ -597,7 +602,7 @@ void fill_zero(T* p, int64_t n, cudaStream_t st) {
   template void reduce_slots<T>(const T*, int64_t, int, int64_t, int64_t, int64_t, T*, int64_t,     \
                                 bool, cudaStream_t);                                                \
   template void softmax_ce_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>, T*, \
-                                double*, double*, cudaStream_t);                                    \
+                                double*, double*, int32_t*, cudaStream_t);                          \
   template void bce_b<T>(const SlotDesc*, int, int, const uint64_t*, int, Act<T>, int, double, Act<T>, \
                          T*, double*, double*, cudaStream_t);                                       \
   template void sgd_step<T>(T*, const T*, int64_t, double, double, cudaStream_t);                   \

@@ -110,7 +110,7 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
 // G (and G_lo when given: TF32-split output, rows [n_batch, max_rows) zeroed)
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
-                  Act<T> G, T* G_lo, double* row_loss, double* loss_out, cudaStream_t st);
+                  Act<T> G, T* G_lo, double* row_loss, double* loss_out, int32_t* nlab, cudaStream_t st);
 // multi-label BCE-with-logits (pos_weight on positives), mean over rows x C; multi-hot
 // targets y (y_words 64-bit words per node); G (+ TF32 G_lo, tail rows zeroed)
 template <typename T>

@@ -26,7 +26,7 @@ inline bool launch_debug() {
 // kernels of the GCN chain (main stream)
 inline bool gcn_kernel(const char* n) {
   static const char* const names[] = {"k_gemm_tc", "k_gemm_b", "k_gather_b", "k_spmm_b", "k_softmax_ce_b",
-                                      "k_loss_mean", "k_reduce_slots", "k_sgd", "k_adam", "k_pad_weights",
+                                      "k_loss_mean", "k_reduce_slots", "k_sgd", "k_adam", "k_split_weights", "k_count_labels",
                                       "k_ledger_add", "k_zero"};
   for (const char* m : names) {
     const char* a = n;
