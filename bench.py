@@ -590,23 +590,25 @@ def _oracle_worker_iter(ctx, it, w):
 
 def cpu_baseline(args, sg, budget_s, saint_norms=None):
     """The oracle port timed on this host: whole worker-iterations until ~budget_s."""
+    from threadpoolctl import threadpool_limits
     ctx = _oracle_setup(args, sg, saint_norms)
     times = []
     t_all = time.perf_counter()
     w = 0
-    while True:
-        t0 = time.perf_counter()
-        _oracle_worker_iter(ctx, 0, w % args.workers)
-        times.append(time.perf_counter() - t0)
-        w += 1
-        if time.perf_counter() - t_all > budget_s and w >= 2:
-            break
+    with threadpool_limits(limits=1):  # one core: BLAS single-threaded too
+        while True:
+            t0 = time.perf_counter()
+            _oracle_worker_iter(ctx, 0, w % args.workers)
+            times.append(time.perf_counter() - t0)
+            w += 1
+            if time.perf_counter() - t_all > budget_s and w >= 2:
+                break
     per_worker = float(np.median(times))
     it_s = 1.0 / (args.workers * per_worker)
     return {"value": round(it_s, 5), "unit": "iters/s", "cores": 1, "kind": "port",
             "sample": f"{len(times)} worker-iterations (plan + fwd/bwd) of the k={args.workers} "
                       f"iteration, median {per_worker:.3f} s; iters/s = 1/(k * median)",
-            "threads_note": f"numpy single-threaded except BLAS; os.cpu_count()={os.cpu_count()}"}
+            "threads_note": f"one thread (BLAS limited by threadpoolctl); os.cpu_count()={os.cpu_count()}"}
 
 
 _REF_CTX = None
@@ -614,6 +616,17 @@ _REF_CTX = None
 
 def _ref_task(a):
     return _oracle_worker_iter(_REF_CTX, a[0], a[1])
+
+
+_REF_LIMITS = None
+
+
+def _ref_worker_init(threads):
+    # BLAS threads per worker process: cores / processes (an unlimited pool per process
+    # oversubscribes the host ~k-fold and runs the reference ~8x slower)
+    global _REF_LIMITS
+    from threadpoolctl import threadpool_limits
+    _REF_LIMITS = threadpool_limits(limits=threads)
 
 
 def run_reference(args):
@@ -635,9 +648,14 @@ def run_reference(args):
     from paper_2101_07706_b200.synth import make_shaped_graph
     sg = make_shaped_graph(args.shape, seed=0, device=None)
     _REF_CTX = _oracle_setup(args, sg)
-    cores = max(1, min(args.workers, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
-                       else (os.cpu_count() or 1)))
-    pool = mp.get_context("fork").Pool(cores) if cores > 1 else None
+    usable = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    procs = max(1, min(args.workers, usable))
+    per_proc = max(1, usable // procs)
+    cores = procs * per_proc
+    pool = (mp.get_context("fork").Pool(procs, initializer=_ref_worker_init, initargs=(per_proc,))
+            if procs > 1 else None)
+    if pool is None:
+        _ref_worker_init(per_proc)
 
     def step(it):
         tasks = [(it, w) for w in range(args.workers)]
@@ -666,8 +684,8 @@ def run_reference(args):
            "impl": "reference",
            "cpu_baseline": {"value": round(it_s, 5), "unit": "iters/s", "cores": cores, "kind": "port",
                             "sample": f"{args.steps} iterations, each the k={args.workers} "
-                                      f"worker-iterations in {cores} parallel processes; "
-                                      "iters/s = 1/mean step time"},
+                                      f"worker-iterations in {procs} parallel processes x "
+                                      f"{per_proc} BLAS threads; iters/s = 1/mean step time"},
            "e2e": {"value": round(it_s, 5), "unit": "iters/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
