@@ -248,8 +248,10 @@ def run_ours(args):
                    sampler=args.sampler, subgraph_size=args.subgraph if saint else None)
     stream = torch.cuda.current_stream()
     n_my = tr.n_my
-    W = max(args.warmup, 1)
     K = ((args.steps + T - 1) // T) * T          # whole look-ahead groups
+    # warm-up: at least the requested steps, in whole groups, and every plan arena used once
+    # (the first group on each arena records its CUDA graphs; none is captured while timed)
+    W = max(args.warmup, 1, tr.n_bufs * T)
     W = ((W + T - 1) // T) * T
     per = tr.per_epoch
 

@@ -47,14 +47,17 @@ bool graphs_on() {
   return on != 0 && g_prof_target.empty();  // per-kernel profiling needs eager launches
 }
 
+// repeat: the caller reuses its keys (Trainer steps, sampler calls): capture at once.
+// Otherwise a key's first use runs eagerly and its second use captures, so one-off calls
+// (loss_and_backward on freshly allocated weights) never pay a capture.
 template <typename Fn>
-int graph_run(GraphCache& gc, const std::string& key, cudaStream_t st, Fn&& launch) {
+int graph_run(GraphCache& gc, const std::string& key, cudaStream_t st, bool repeat, Fn&& launch) {
   auto it = gc.map.find(key);
   if (it == gc.map.end()) {
-    // a key's first use runs eagerly: one-off calls (e.g. loss_and_backward on freshly
-    // allocated weights) never pay a capture; the second use captures
-    if (gc.seen.size() > 4096) gc.seen.clear();
-    if (gc.seen[key]++ == 0) return launch(st);
+    if (!repeat) {
+      if (gc.seen.size() > 4096) gc.seen.clear();
+      if (gc.seen[key]++ == 0) return launch(st);
+    }
     if (!gc.cap && cudaStreamCreateWithFlags(&gc.cap, cudaStreamNonBlocking) != cudaSuccess) {
       set_error("graph capture stream");
       return SKG_ERR_CUDA;
@@ -262,7 +265,7 @@ int run_ladies(skg_plans* ps, int n, int max_upper, cudaStream_t st) {
   key_put(key, n);
   key_put(key, max_upper);
   key_put(key, c->gen);
-  return graph_run(ps->graphs, key, st, launch);
+  return graph_run(ps->graphs, key, st, true, launch);
 }
 
 struct skg_gcn {
@@ -1524,13 +1527,13 @@ std::string graph_key(const skg_gcn* g, int z0, int n, const uint64_t* wp, const
 }
 
 int gcn_dispatch(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, bool acc,
-                 double* loss, bool backward, cudaStream_t st) {
+                 double* loss, bool backward, cudaStream_t st, bool repeat = false) {
   int rc = refresh_batches(g, z0, n, st);
   if (rc) return rc;
   if (backward && loss && gp && graphs_on()) {
     // training step: replay a CUDA graph of its ~45 launches
     if (!g->loss_scratch) CK(cudaMalloc(&g->loss_scratch, sizeof(double) * std::max(g->n_slots, 1)));
-    rc = graph_run(g->graphs, graph_key(g, z0, n, wp, gp, acc), st, [&](cudaStream_t cs) {
+    rc = graph_run(g->graphs, graph_key(g, z0, n, wp, gp, acc), st, repeat, [&](cudaStream_t cs) {
       return gcn_eager(g, z0, n, wp, gp, acc, g->loss_scratch, true, cs);
     });
     if (rc) return rc;
@@ -1564,8 +1567,9 @@ extern "C" int skg_gcn_step_batch(skg_gcn* g, int slot0, int n, const uint64_t* 
       "bad gcn_step_batch arguments");
   ARG(g->ps->ctx->d_labels || g->ps->ctx->d_ymulti, "labels not set");
   CK(cudaSetDevice(g->ps->ctx->device));
+  // the batched step is the Trainer's: its keys repeat every group
   return gcn_dispatch(g, slot0, n, wp, gp, accumulate != 0, (double*)loss_dev, true,
-                      (cudaStream_t)stream);
+                      (cudaStream_t)stream, true);
 }
 
 extern "C" int skg_gcn_forward(skg_gcn* g, int slot, const uint64_t* wp, void* stream) {
