@@ -57,7 +57,7 @@ def parse():
     ap.add_argument("--lr", type=float, default=0.0, help="0: 0.5 (LADIES), 0.05 (GraphSAINT)")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ahead", type=int, default=4, help="iterations of plans per sampler launch")
+    ap.add_argument("--ahead", type=int, default=3, help="iterations of plans per sampler launch")
     ap.add_argument("--streams", type=int, default=2, help="sampler streams (groups in flight)")
     a = ap.parse_args()
     if a.sampler == "auto":

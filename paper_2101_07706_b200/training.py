@@ -801,7 +801,7 @@ class Trainer:
 def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, cfg: SamplerConfig, *,
                       epochs: int, batch_size: int, lr: float, mode: str, seed: int,
                       sampler: str = "ladies", subgraph_size: int | None = None,
-                      optimizer: str = "sgd", ahead: int = 4, streams: int = 2,
+                      optimizer: str = "sgd", ahead: int = 3, streams: int = 2,
                       pos_weight: float = 50.0) -> tuple:
     """Data-parallel training with per-iteration gradient averaging (training.py:430-518).
 
