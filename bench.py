@@ -352,8 +352,11 @@ def run_ours(args):
     remote_per_iter = float(ledger.sum().item()) / (W + K)
     torch.cuda.synchronize()
     stats = [tr.bufs[0][0].stats(i)[0] for i in range(n_my * T)]
-    s0_remote = sum(int(st[N_LAYERS - 1, 4]) for st in stats) / T   # input-layer rows moved
-    sampled_nodes = sum(int(st[:, 2].sum()) for st in stats) / T
+    # GraphSAINT plans record their one subgraph (shared by every GCN layer) as layer 0
+    in_layer = 0 if saint else N_LAYERS - 1
+    s0_remote = sum(int(st[in_layer, 4]) for st in stats) / T   # input-layer rows moved
+    sampled_nodes = (sum(int(st[0, 2]) for st in stats) if saint
+                     else sum(int(st[:, 2].sum()) for st in stats)) / T
     alg_bytes = sum(algorithmic_sampler_bytes(st, saint) for st in stats)   # one T-plan launch
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
     samp_ms, comp_ms = [], []
@@ -391,7 +394,7 @@ def run_ours(args):
     t_s0 = time.perf_counter()
     steps_serial(W, K)
     serial_ms = (time.perf_counter() - t_s0) * 1e3  # host-timed: every group ends in a sync
-    kern = kernel_table(lib, steps_serial, W, K, stats, tr, n_my, T, peaks)
+    kern = kernel_table(lib, steps_serial, W, K, stats, tr, n_my, T, peaks, saint)
     top = max(kern, key=lambda r: r["total_ms"])
 
     # ---- e2e through the public API: host-derived inputs, H2D each step, loss D2H
@@ -497,7 +500,7 @@ def run_ours(args):
     return out
 
 
-def kernel_table(lib, steps_fn, W, K, stats, tr, n_my, T, peaks):
+def kernel_table(lib, steps_fn, W, K, stats, tr, n_my, T, peaks, saint=False):
     """Event-time the main kernels over the K timed steps (replayed by steps_fn) and relate
     each to its algorithmic bytes (HBM-bound sampler kernels) or flops (tensor-core GEMM)."""
     import torch
@@ -508,7 +511,7 @@ def kernel_table(lib, steps_fn, W, K, stats, tr, n_my, T, peaks):
     R = sum(int(st[t, 0]) for st in stats for t in range(L))
     Nc = sum(int(st[t, 1]) for st in stats for t in range(L))
     E = sum(int(st[t, 9]) for st in stats for t in range(L))
-    launches_per_group = L  # one launch per layer for each sampler kernel
+    launches_per_group = 1 if saint else L  # sampler launches per group (GraphSAINT: one subgraph)
     models = {  # bytes per sampler launch (averaged over the layers of one group)
         "k_lad_expand": (4 * E + 16 * R) / launches_per_group,
         "k_lad_scatter": (8 * E + 16 * R) / launches_per_group,
@@ -518,7 +521,9 @@ def kernel_table(lib, steps_fn, W, K, stats, tr, n_my, T, peaks):
     }
     # GEMM flops per launch: 3 contractions per layer (no input-gradient GEMM at layer 0)
     dims = tr.dims
-    rows = [sum(int(st[L - 1 - l, 0]) for st in stats) / T for l in range(L)]  # per iteration
+    # rows of each GCN layer per iteration: LADIES layer l consumes sampled set S_{L-1-l};
+    # a GraphSAINT subgraph (recorded as layer 0) serves every layer
+    rows = [sum(int(st[0 if saint else L - 1 - l, 0]) for st in stats) / T for l in range(L)]
     gflop = sum(2 * rows[l] * dims[l] * dims[l + 1] * (3 if l > 0 else 2) for l in range(L))
     n_gemm = 3 * L - 1
     out = []
