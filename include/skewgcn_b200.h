@@ -48,6 +48,12 @@ int skg_device_count(void);
  * stream until skg_profile_stop, which synchronises and returns the summed time. */
 int skg_profile_start(const char* kernel_name);
 int skg_profile_stop(double* total_ms, int64_t* launches);
+/* With kernel_name "*": every launch is bracketed; skg_profile_table then writes one
+ * "name launches total_ms" line per launch name (template-qualified for the GEMMs). */
+int skg_profile_table(char* out, int64_t cap);
+/* Capture-only mode: launch sequences replayed as CUDA graphs (the LADIES sampler and the
+ * batched training step) are captured and instantiated but not replayed while it is on. */
+int skg_set_capture_only(int on);
 
 /* ---------------------------------------------------------------- host RNG runtime
  * spawn_rng (seeding.py:17-27): SHA-256 of each label's repr -> SeedSequence -> PCG64.
@@ -133,6 +139,11 @@ int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, int mode,
 /* CommLedger.add_plan (training.py:127-128) on device: ledger_dev is int64 [k x n_layers]
  * (one epoch); adds remote_per_layer of slots [slot0, slot0+n) to their workers' rows. */
 int skg_plans_ledger_add(skg_plans* ps, int slot0, int n, uint64_t ledger_dev, void* stream);
+/* Sticky error state of a plan set: the err bits of every plan passed to
+ * skg_plans_ledger_add since the last clear (sampling errors, and "batch contains no
+ * labeled nodes" from its training step), which later sampling calls cannot erase.
+ * Synchronises; returns the matching status (SKG_OK when clean). */
+int skg_plans_sticky_error(skg_plans* ps, int clear);
 /* Synchronous readback.  stats: n_layers x 16 int64 (doubles bit-cast):
  * [n_upper, n_cand, n_nodes, nnz, remote, has_dist, n_remote_cand, starved, skew,
  *  n_pairs, kept_pairs, s, total, T, pw_depth, 0]; info: [err_bits, draws_consumed,

@@ -255,12 +255,44 @@ def read_layer(ps: PlanSet, slot: int, t: int, st_row: np.ndarray, want_dist: bo
     return out
 
 
+_RANK_LIMIT = 65535  # LADIES plans keep upper-row ranks / pair counters in 16 bits
+
+
+def _pow2(x: int) -> int:
+    return 1 << max(0, int(x) - 1).bit_length()
+
+
+def query_chunks(g, s: np.ndarray):
+    """Split a sorted row set into consecutive runs a saturated one-layer plan can hold
+    (rows and the sum of their degrees both below the 16-bit rank limit)."""
+    deg = np.diff(np.asarray(g.offsets))[s]
+    if len(s) and int(deg.max()) >= _RANK_LIMIT:
+        raise ValueError("a row's degree exceeds the device query limit (65534)")
+    out, lo, acc = [], 0, 0
+    for i, d in enumerate(deg.tolist()):
+        if i > lo and (acc + d >= _RANK_LIMIT or i - lo >= _RANK_LIMIT - 1):
+            out.append(s[lo:i])
+            lo, acc = i, 0
+        acc += d
+    if len(s):
+        out.append(s[lo:])
+    return out
+
+
 def one_layer(g, s: np.ndarray) -> dict:
-    """Saturated single-layer plan over upper set s: N(s), column norms, block (p = 1)."""
+    """Saturated single-layer plan over upper set s: N(s), column norms, block (p = 1).
+    The budget is min(n, sum of deg(s)) >= |N(s)|, so the layer never draws; callers
+    split row sets beyond the 16-bit rank limit with ``query_chunks``."""
     import scipy.sparse as sp
     dg = device_graph(g)
-    budget = max(int(g.n_nodes), 1)
-    ps = dg.acquire(KIND_LADIES, 1, 1, budget, max(len(s), 1))
+    bound = int(np.diff(np.asarray(g.offsets))[s].sum()) if len(s) else 1
+    budget = max(1, min(int(g.n_nodes), bound))
+    if max(budget, len(s)) >= _RANK_LIMIT:
+        raise ValueError("row set too large for one device query; split it with query_chunks")
+    # pooled arenas are keyed by shape: round to powers of two so repeated queries of
+    # different sizes share a few arenas
+    budget_k = min(_pow2(budget), _RANK_LIMIT - 1, max(int(g.n_nodes), 1))
+    ps = dg.acquire(KIND_LADIES, 1, 1, budget_k, min(_pow2(max(len(s), 1)), _RANK_LIMIT - 1))
     try:
         off = np.array([0, len(s)], dtype=np.int64)
         ids = np.ascontiguousarray(s, dtype=np.int64)

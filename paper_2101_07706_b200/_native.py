@@ -45,6 +45,8 @@ _sig("skg_kernel_launches", C.c_ulonglong)
 _sig("skg_device_count", C.c_int)
 _sig("skg_profile_start", C.c_int, C.c_char_p)
 _sig("skg_profile_stop", C.c_int, P(dbl), P(i64))
+_sig("skg_profile_table", C.c_int, C.c_char_p, i64)
+_sig("skg_set_capture_only", C.c_int, C.c_int)
 _sig("skg_spawn_pcg64", C.c_int, u64, P(C.c_char_p), C.c_int, P(u64))
 _sig("skg_choice_noreplace", C.c_int, P(u64), C.c_int, C.c_uint32, i64, i64, P(i64))
 _sig("skg_iteration_inputs", C.c_int, u64, i64, i64, i64, P(i64), i64, i64, P(i64), P(i64), P(u64))
@@ -60,6 +62,7 @@ _sig("skg_gcn_set_loss", C.c_int, vp, C.c_int, C.c_double)
 _sig("skg_ctx_info", C.c_int, vp, P(i64))
 _sig("skg_ctx_set_owner", C.c_int, vp, i32, P(i32))
 _sig("skg_plans_ledger_add", C.c_int, vp, C.c_int, C.c_int, u64, vp)
+_sig("skg_plans_sticky_error", C.c_int, vp, C.c_int)
 _sig("skg_ipc_handle", C.c_int, u64, P(C.c_uint8))
 _sig("skg_ipc_open", C.c_int, P(C.c_uint8), P(u64))
 _sig("skg_ipc_close", C.c_int, u64)
@@ -92,10 +95,10 @@ _sig("skg_set_gemm_mode", C.c_int, C.c_int)
 # every symbol the public header declares (checked by tests/test_native_abi.py)
 EXPORTED = [
     "skg_abi_version", "skg_last_error", "skg_kernel_launches", "skg_device_count",
-    "skg_profile_start", "skg_profile_stop",
+    "skg_profile_start", "skg_profile_stop", "skg_profile_table", "skg_set_capture_only",
     "skg_spawn_pcg64", "skg_choice_noreplace", "skg_iteration_inputs", "skg_ctx_create",
     "skg_ctx_destroy", "skg_ctx_set_features", "skg_ctx_set_feature_map", "skg_ctx_feature_ptr", "skg_ctx_shard_upload",
-    "skg_ctx_set_labels", "skg_ctx_set_multilabels", "skg_gcn_set_loss", "skg_ctx_set_owner", "skg_ctx_info", "skg_plans_ledger_add", "skg_ipc_handle", "skg_ipc_open", "skg_ipc_close",
+    "skg_ctx_set_labels", "skg_ctx_set_multilabels", "skg_gcn_set_loss", "skg_ctx_set_owner", "skg_ctx_info", "skg_plans_ledger_add", "skg_plans_sticky_error", "skg_ipc_handle", "skg_ipc_open", "skg_ipc_close",
     "skg_plans_create", "skg_plans_destroy", "skg_ladies_sample", "skg_ladies_sample_device", "skg_saint_set_candidates", "skg_column_norms_pull",
     "skg_saint_sample", "skg_plan_stats", "skg_plan_layer", "skg_gcn_create", "skg_gcn_destroy",
     "skg_gcn_step", "skg_gcn_step_batch", "skg_gcn_forward", "skg_gcn_read_logits", "skg_predict_logits",

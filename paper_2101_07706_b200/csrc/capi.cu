@@ -17,10 +17,24 @@
 #include "skg_internal.h"
 
 namespace skg {
+// per-kernel event timing (bench.py roofline): target "*" brackets every launch, else the
+// launches whose name equals the target; pairs are kept per launch name
 static std::string g_prof_target;
-static std::vector<std::pair<cudaEvent_t, cudaEvent_t>> g_prof_pairs;
+struct ProfPair {
+  std::string name;
+  cudaEvent_t a, b;
+};
+static std::vector<ProfPair> g_prof_pairs;
 static cudaEvent_t g_prof_open = nullptr;
-bool prof_match(const char* name) { return !g_prof_target.empty() && g_prof_target == name; }
+static std::string g_prof_open_name;
+bool prof_match(const char* name) {
+  if (g_prof_target.empty()) return false;
+  if (g_prof_target == "*" || g_prof_target == name) {
+    g_prof_open_name = name;
+    return true;
+  }
+  return false;
+}
 
 // CUDA graphs of fixed launch sequences (the training step, the LADIES sampler): the
 // per-call host cost of ~50-90 launches was the throughput limit.  A sequence is captured
@@ -42,6 +56,11 @@ struct GraphCache {
   }
 };
 
+// capture-only mode (skg_set_capture_only): graph_run records and instantiates a launch
+// sequence without replaying it, so a benchmark can build every graph it will replay
+// before its warm-up (no capture inside a timed region, warm-up exactly as requested)
+static int g_capture_only = 0;
+
 bool graphs_on() {
   static const int on = getenv("SKG_GCN_GRAPH") ? atoi(getenv("SKG_GCN_GRAPH")) : 1;
   return on != 0 && g_prof_target.empty();  // per-kernel profiling needs eager launches
@@ -54,7 +73,7 @@ template <typename Fn>
 int graph_run(GraphCache& gc, const std::string& key, cudaStream_t st, bool repeat, Fn&& launch) {
   auto it = gc.map.find(key);
   if (it == gc.map.end()) {
-    if (!repeat) {
+    if (!repeat && !g_capture_only) {
       if (gc.seen.size() > 4096) gc.seen.clear();
       if (gc.seen[key]++ == 0) return launch(st);
     }
@@ -93,6 +112,7 @@ int graph_run(GraphCache& gc, const std::string& key, cudaStream_t st, bool repe
     }
     it = gc.map.emplace(key, GraphEntry{exec, nl}).first;
   }
+  if (g_capture_only) return SKG_OK;
   if (cudaGraphLaunch(it->second.exec, st) != cudaSuccess) {
     set_error(std::string("graph launch: ") + cudaGetErrorString(cudaGetLastError()));
     return SKG_ERR_CUDA;
@@ -110,7 +130,7 @@ void prof_record(cudaStream_t st, bool before) {
   cudaEventCreate(&e);
   cudaEventRecord(e, st);
   if (before) g_prof_open = e;
-  else g_prof_pairs.push_back({g_prof_open, e});
+  else g_prof_pairs.push_back({g_prof_open_name, g_prof_open, e});
 }
 static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
@@ -220,6 +240,9 @@ struct skg_plans {
   std::vector<int64_t> n_local;
   std::vector<bool> local_norm_ready;
   GraphCache graphs;  // LADIES launch sequences per (plans, rows cap, context generation)
+  // sticky error bits: every consumed plan's err word is OR-ed in by k_ledger_add (after
+  // its training step), so an error survives the arena's reuse by the next sampling call
+  int32_t* d_sticky = nullptr;
   // pinned staging of each sampling call's uploads (descriptors, batch ids); up_ev marks
   // the last upload consumed by its stream before the host rewrites the staging
   PlanDev* h_pin = nullptr;
@@ -362,15 +385,52 @@ extern "C" int skg_profile_stop(double* total_ms, int64_t* launches) {
   double tot = 0.0;
   for (auto& pr : g_prof_pairs) {
     float ms = 0.f;
-    cudaEventElapsedTime(&ms, pr.first, pr.second);
+    cudaEventElapsedTime(&ms, pr.a, pr.b);
     tot += ms;
-    cudaEventDestroy(pr.first);
-    cudaEventDestroy(pr.second);
+    cudaEventDestroy(pr.a);
+    cudaEventDestroy(pr.b);
   }
   *total_ms = tot;
   *launches = (int64_t)g_prof_pairs.size();
   g_prof_pairs.clear();
   g_prof_target.clear();
+  return SKG_OK;
+}
+
+// per launch name: "name launches total_ms\n" lines into out (truncated to cap bytes)
+extern "C" int skg_profile_table(char* out, int64_t cap) {
+  ARG(out && cap > 0, "bad profile buffer");
+  CK(cudaDeviceSynchronize());
+  std::vector<std::string> order;
+  std::unordered_map<std::string, std::pair<int64_t, double>> acc;
+  for (auto& pr : g_prof_pairs) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, pr.a, pr.b);
+    cudaEventDestroy(pr.a);
+    cudaEventDestroy(pr.b);
+    auto it = acc.find(pr.name);
+    if (it == acc.end()) {
+      order.push_back(pr.name);
+      it = acc.emplace(pr.name, std::make_pair((int64_t)0, 0.0)).first;
+    }
+    it->second.first += 1;
+    it->second.second += ms;
+  }
+  std::string txt;
+  char line[512];
+  for (auto& nm : order) {
+    snprintf(line, sizeof(line), "%s %lld %.6f\n", nm.c_str(), (long long)acc[nm].first, acc[nm].second);
+    txt += line;
+  }
+  g_prof_pairs.clear();
+  g_prof_target.clear();
+  const size_t n = std::min<size_t>(txt.size(), (size_t)cap - 1);
+  memcpy(out, txt.data(), n);
+  out[n] = 0;
+  return SKG_OK;
+}
+extern "C" int skg_set_capture_only(int on) {
+  g_capture_only = on ? 1 : 0;
   return SKG_OK;
 }
 extern "C" const char* skg_last_error(void) { return last_error(); }
@@ -832,6 +892,8 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
   }
   CK(cudaMalloc(&ps->d_plans, sizeof(PlanDev) * n_slots));
   CK(cudaMemcpy(ps->d_plans, ps->h.data(), sizeof(PlanDev) * n_slots, cudaMemcpyHostToDevice));
+  CK(cudaMalloc(&ps->d_sticky, sizeof(int32_t)));
+  CK(cudaMemset(ps->d_sticky, 0, sizeof(int32_t)));
   *out = ps;
   return SKG_OK;
 }
@@ -850,6 +912,7 @@ extern "C" int skg_plans_destroy(skg_plans* ps) {
   cudaFree(ps->arena);
   cudaFree(ps->d_scal);
   cudaFree(ps->d_plans);
+  cudaFree(ps->d_sticky);
   cudaFree(ps->d_train);
   cudaFree(ps->d_train_norm);
   cudaFree(ps->d_train_bitmap);
@@ -1131,9 +1194,10 @@ extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, in
                       (int)ps->budget, st);
 }
 
-__global__ void k_ledger_add(const PlanDev* plans, int L, int64_t* ledger) {
+__global__ void k_ledger_add(const PlanDev* plans, int L, int64_t* ledger, int32_t* sticky) {
   SKG_PDL_PROLOGUE();
   const PlanDev& P = plans[blockIdx.x];
+  if (threadIdx.x == 0 && *P.err) atomicOr(sticky, *P.err);
   for (int t = threadIdx.x; t < L; t += blockDim.x) {
     // reference layer order is bottom-up: layer l <-> top-down t = L-1-l (LADIES);
     // SAINT charges its remote count at layer 0 only (training.py:248-253)
@@ -1153,9 +1217,22 @@ extern "C" int skg_plans_ledger_add(skg_plans* ps, int slot0, int n, uint64_t le
                                     void* stream) {
   ARG(ps && slot0 >= 0 && n >= 1 && slot0 + n <= ps->n_slots && ledger_dev, "bad ledger arguments");
   cudaStream_t st = (cudaStream_t)stream;
-  launch_k("k_ledger_add", st, dim3(n), dim3(32), 0, k_ledger_add, ps->d_plans + slot0, ps->L, (int64_t*)ledger_dev);
+  launch_k("k_ledger_add", st, dim3(n), dim3(32), 0, k_ledger_add, ps->d_plans + slot0, ps->L, (int64_t*)ledger_dev,
+           ps->d_sticky);
   CK(cudaGetLastError());
   return SKG_OK;
+}
+
+// errors of every plan consumed since the last clear (sampling errors and the training
+// step's "no labeled nodes"), which later sampling calls into the arena cannot erase
+extern "C" int skg_plans_sticky_error(skg_plans* ps, int clear) {
+  ARG(ps, "null plan set");
+  CK(cudaSetDevice(ps->ctx->device));
+  CK(cudaDeviceSynchronize());
+  int32_t err = 0;
+  CK(cudaMemcpy(&err, ps->d_sticky, sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (clear) CK(cudaMemset(ps->d_sticky, 0, sizeof(int32_t)));
+  return status_from_err(err);
 }
 
 extern "C" int skg_plan_stats(skg_plans* ps, int slot, int64_t* stats, int64_t info[4]) {
@@ -1436,6 +1513,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     Act<T> Hn = act<T>(g->H[l + 1], R, g->ld[l + 1], g->ld[l + 1], z0);
     if constexpr (F32) {
       if (tc) {
+        g_gemm_layer = l;
         rc = gemm_tc(mode, false, false, n, Ri, (int)g->dims[l + 1], (int)g->dims[l], rows, nullptr,
                      op(g->U[l], g->Ulo[l], g->ld[l], g->ld[l]), wop(l), Hn, false, st);
         if (rc) return rc;
@@ -1445,6 +1523,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     gemm_simt<T>(false, false, n, Ri, (int)g->dims[l + 1], (int)g->dims[l], rows, nullptr, U, W(l), Hn,
                  false, st);
   }
+  g_gemm_layer = -1;
   if (!backward) return SKG_OK;
   Act<T> G = act<T>(g->G0, R, g->ld_max, g->ld[L], z0);
   Act<T> Gu = act<T>(g->G1, R, g->ld_max, g->ld[L], z0);
@@ -1473,6 +1552,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     int ks = 1;  // K split inside each slot: partial (slot, run) blocks in slot-major order
     if constexpr (F32) {
       if (tc) {
+        g_gemm_layer = l;
         ks = gemm_tc_ksplit(n, dl, dn, Ri);
         rc = gemm_tc(mode, true, false, n, dl, dn, Ri, nullptr, rows, op(g->U[l], g->Ulo[l], g->ld[l], g->ld[l]),
                      op(g->G0, g->G0lo, g->ld_max, G.ld), P, false, st, ks);
@@ -1503,6 +1583,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
               g->ld[l], st);
     G = Gn;
   }
+  g_gemm_layer = -1;
   return SKG_OK;
 }
 

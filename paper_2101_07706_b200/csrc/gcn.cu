@@ -175,9 +175,9 @@ template <typename T>
 void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
             Act<T> H, Act<T> out, T* out_lo, int64_t width, cudaStream_t st) {
   dim3 grid(row_blocks(max_rows, n), n);
-  if (transposed) launch_k("k_spmm_b", st, dim3(grid), dim3(256), 0, k_spmm_b<T, true, false>, ld, A, H, out, out_lo, max_rows, width);
-  else if (relu_in) launch_k("k_spmm_b", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, true>, ld, A, H, out, out_lo, max_rows, width);
-  else launch_k("k_spmm_b", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, false>, ld, A, H, out, out_lo, max_rows, width);
+  if (transposed) launch_k("k_spmm_b<T,1,0>", st, dim3(grid), dim3(256), 0, k_spmm_b<T, true, false>, ld, A, H, out, out_lo, max_rows, width);
+  else if (relu_in) launch_k("k_spmm_b<F,1>", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, true>, ld, A, H, out, out_lo, max_rows, width);
+  else launch_k("k_spmm_b<F,0>", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, false>, ld, A, H, out, out_lo, max_rows, width);
 }
 
 // full-graph SpMM for predict_logits (int64 offsets)

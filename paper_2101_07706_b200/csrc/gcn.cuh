@@ -78,6 +78,7 @@ extern int g_ksplit_override;
 // ks > 1 splits every slot's K into ks contiguous runs of 32-wide chunks: output block
 // z * ks + j holds run j of slot z (partials for a fixed-order reduction).
 constexpr int kMaxKSplit = 4;
+extern thread_local int g_gemm_layer;
 int gemm_tc(int mode, bool ta, bool tb, int n, int M, int N, int K, const int32_t* const* dM,
             const int32_t* const* dK, const TcOp& A, const TcOp& B, Act<float> C, bool acc,
             cudaStream_t st, int ks = 1);

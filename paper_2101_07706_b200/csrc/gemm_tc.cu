@@ -622,6 +622,10 @@ int op_maps(const TcOp& op, bool mn, int64_t mn_extent, int64_t k_extent, int ro
 
 }  // namespace
 
+// GCN layer of the GEMM being launched (set by the training step; -1 elsewhere): launch
+// names carry it ("k_gemm_tc<...>@l2") so per-kernel profiles can attribute flops
+thread_local int g_gemm_layer = -1;
+
 static int sm_count() {
   static int n = 0;
   if (!n) {
@@ -659,7 +663,10 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
       pattr = true;
     }
     const int grid_p = (int)std::min<long long>(tiles, sm_count());
-    launch_k("k_gemm_tc", st, dim3(grid_p), dim3(tc::NTHREADS), CF::SMEM, pk, maps, M, N, K, dM, dK, as, bs, C,
+    static const std::string pname = "k_gemm_tc_p<" + std::to_string((int)TA) + "," + std::to_string((int)TB) + "," +
+                                     std::to_string(BN) + "," + std::to_string(MODE) + ">";
+    const std::string pn = g_gemm_layer >= 0 ? pname + "@l" + std::to_string(g_gemm_layer) : pname;
+    launch_k(pn.c_str(), st, dim3(grid_p), dim3(tc::NTHREADS), CF::SMEM, pk, maps, M, N, K, dM, dK, as, bs, C,
              acc ? 1 : 0, ks, tn, tm, (int)tiles);
     return SKG_OK;
   }
@@ -670,7 +677,10 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
     attr = true;
   }
   dim3 grid(tn, tm, n * ks);
-  launch_k("k_gemm_tc", st, dim3(grid), dim3(tc::NTHREADS), CF::SMEM, kern, maps, M, N, K, dM, dK, as, bs, C,
+  static const std::string kname = "k_gemm_tc<" + std::to_string((int)TA) + "," + std::to_string((int)TB) + "," +
+                                   std::to_string(BN) + "," + std::to_string(MODE) + ">";
+  const std::string kn = g_gemm_layer >= 0 ? kname + "@l" + std::to_string(g_gemm_layer) : kname;
+  launch_k(kn.c_str(), st, dim3(grid), dim3(tc::NTHREADS), CF::SMEM, kern, maps, M, N, K, dM, dK, as, bs, C,
            acc ? 1 : 0, ks);
   return SKG_OK;
 }

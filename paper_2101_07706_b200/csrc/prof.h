@@ -32,7 +32,7 @@ inline bool gcn_kernel(const char* n) {
     const char* a = n;
     const char* b = m;
     while (*a && *a == *b) ++a, ++b;
-    if (*a == 0 && *b == 0) return true;
+    if ((*a == 0 || *a == '<') && *b == 0) return true;  // template-qualified launch names
   }
   return false;
 }

@@ -240,13 +240,21 @@ def save_dataset(g: WeightedGraph, directory) -> None:
 def load_partition_csv(path, n_nodes: int, k: int) -> Partition:
     """Explicit "node,worker" assignment covering every node (partition.py:77-98)."""
     owner = np.full(n_nodes, -1, dtype=np.int64)
-    for node, worker in _pairs(path, "node,worker"):
-        w = int(worker)
-        if not 0 <= node < n_nodes:
-            raise ValueError(f"{path}: node {node} out of range")
-        if not 0 <= w < k:
-            raise ValueError(f"{path}: worker {w} out of range")
-        owner[node] = w
+    # rows are validated in file order, so the first bad line wins, as in the reference
+    with Path(path).open("r", encoding="utf-8") as fh:
+        for lineno, parts in enumerate(csv.reader(fh), start=1):
+            if not parts:
+                continue
+            if lineno == 1 and not parts[0].strip().lstrip("-").isdigit():
+                continue
+            if len(parts) != 2:
+                raise ValueError(f"{path}:{lineno}: expected 'node,worker'")
+            node, w = int(parts[0]), int(parts[1])
+            if not 0 <= node < n_nodes:
+                raise ValueError(f"{path}:{lineno}: node {node} out of range")
+            if not 0 <= w < k:
+                raise ValueError(f"{path}:{lineno}: worker {w} out of range")
+            owner[node] = w
     missing = np.flatnonzero(owner < 0)
     if len(missing):
         raise ValueError(f"partition file misses nodes {missing[:10].tolist()}")

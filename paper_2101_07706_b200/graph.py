@@ -165,11 +165,12 @@ def from_shaped(sg) -> WeightedGraph:
 
 def neighbor_union(g: WeightedGraph, s) -> np.ndarray:
     """N(s) = union of adjacency rows of s, sorted (graph.py:186-195), on the GPU."""
-    from ._device import one_layer
+    from ._device import one_layer, query_chunks
     s = check_node_set(s, g.n_nodes)
     if len(s) == 0:
         return np.zeros(0, dtype=np.int64)
-    return one_layer(g, s)["cand"].astype(np.int64)
+    parts = [one_layer(g, c)["cand"].astype(np.int64) for c in query_chunks(g, s)]
+    return parts[0] if len(parts) == 1 else np.unique(np.concatenate(parts))
 
 
 _PUSH_MAX_ROWS = 16384  # row sets above this use the pull formulation
@@ -184,7 +185,10 @@ def column_norms(g: WeightedGraph, s_l, candidates) -> np.ndarray:
         if len(candidates):
             raise ValueError("candidates must be empty when s_l is empty")
         return np.zeros(0)
-    if len(s_l) > _PUSH_MAX_ROWS:  # pull formulation: no per-call plan, any row count
+    from ._device import query_chunks
+    if len(s_l) > _PUSH_MAX_ROWS or len(query_chunks(g, s_l)) > 1:
+        # pull formulation: no per-call plan, any row count (a push plan holds < 2^16 pairs'
+        # row ranks, and splitting the rows would reorder the np.add.at fold)
         from ._device import device_graph
         from ._native import check, lib, ptr
         import ctypes as C
@@ -209,11 +213,17 @@ def column_norms(g: WeightedGraph, s_l, candidates) -> np.ndarray:
 
 def adjacency_block(g: WeightedGraph, rows, cols) -> sp.csr_matrix:
     """w[i, j] for i in rows, j in cols (graph.py:223-242); block built on the GPU."""
-    from ._device import one_layer
+    from ._device import query_chunks
     rows = check_node_set(rows, g.n_nodes)
     cols = check_node_set(cols, g.n_nodes)
     if len(rows) == 0 or len(cols) == 0:
         return sp.csr_matrix((len(rows), len(cols)))
+    parts = [_block_rows(g, c, cols) for c in query_chunks(g, rows)]
+    return parts[0] if len(parts) == 1 else sp.vstack(parts, format="csr")
+
+
+def _block_rows(g: WeightedGraph, rows, cols) -> sp.csr_matrix:
+    from ._device import one_layer
     lay = one_layer(g, rows)
     full = lay["block"]                       # rows x N(rows), values w (p = 1)
     cand = lay["cand"].astype(np.int64)

@@ -601,6 +601,8 @@ class Trainer:
         self._bids = np.zeros(n_slots * max(1, batch_size), dtype=np.int64)
         self._len = C.c_int64()
         self._group = []  # (epoch, it) of the sampled-ahead slot groups
+        self._pending = []  # (group, arena) sampled ahead of the next pipeline call
+        self._gseq = 0      # groups sampled so far (arena = _gseq % n_bufs)
 
     # -- sharded features over NVLink (one process per GPU) ------------------
     def _install_feature_shards(self):
@@ -736,46 +738,84 @@ class Trainer:
                                     float(self.lr), contrib, self.t, self.stream))
 
     def iteration(self, epoch, it):
+        self.drop_pending()
         self.sample_group([(epoch, it)], 0)
         self.wait_sampled(0)
         self.compute(epoch, it, 0, 0)
         self.reduce_and_step()
         self.release_buf(0)
 
-    def pipeline(self, n_groups, sample_fn, compute_fn):
-        """Drive groups 0..n_groups-1: group g is sampled into arena g % n_bufs on sampler
-        stream g % n_streams up to n_streams groups ahead of the GCN, which consumes the
-        groups in order on the main stream (``sample_fn(g, buf)``, ``compute_fn(g, buf)``)."""
-        if n_groups <= 0:
-            return
+    def pipeline(self, groups, sample_fn, compute_fn, next_groups=()):
+        """Drive ``groups`` (hashable descriptors) in order: each is sampled into the next
+        plan arena (round robin over ``n_bufs``) on that arena's sampler stream, up to
+        ``n_streams`` groups ahead of the GCN, which consumes them in order on the main
+        stream (``sample_fn(desc, buf)``, ``compute_fn(desc, buf)``).
+
+        The look-ahead carries over between calls: after the last group, the first
+        ``n_streams`` of ``next_groups`` are sampled too and kept pending, and a later call
+        whose groups start with them computes them without sampling them again.  A run of
+        calls is therefore one continuous pipeline (steady state across call boundaries)."""
         S, NB = self.n_streams, self.n_bufs
-        for g in range(min(S, n_groups)):
-            sample_fn(g, g % NB)
-        for g in range(n_groups):
-            b = g % NB
+        groups = list(groups)
+        queue = groups + list(next_groups)[:S]
+        done = []
+        for desc, buf in self._pending:  # sampled ahead by the previous call
+            if len(done) < len(queue) and queue[len(done)] == desc:
+                done.append((desc, buf))
+            else:
+                break
+        self._pending = []
+
+        def sample_next():
+            desc = queue[len(done)]
+            buf = self._gseq % NB
+            self._gseq += 1
+            sample_fn(desc, buf)
+            done.append((desc, buf))
+
+        while len(done) < min(S, len(queue)):
+            sample_next()
+        for g in range(len(groups)):
+            desc, b = done[g]
             self.wait_sampled(b)
-            compute_fn(g, b)
+            compute_fn(desc, b)
             self.release_buf(b)
-            if g + S < n_groups:  # its arena was used by group g - 1, released above
-                sample_fn(g + S, (g + S) % NB)
+            if len(done) < len(queue):  # its arena was used by group g - 1, released above
+                sample_next()
+        self._pending = done[len(groups):]
 
-    def run(self, pairs, on_iteration=None):
+    def drop_pending(self):
+        """Forget plans sampled ahead (before a caller drives the arenas directly)."""
+        self._pending = []
+
+    def run(self, pairs, on_iteration=None, next_pairs=()):
         """Train over iterations ``pairs`` in order, ``ahead`` iterations of plans per
-        sampling launch, sampled ahead of the GCN on the sampler streams."""
-        groups = [pairs[g0:g0 + self.ahead] for g0 in range(0, len(pairs), self.ahead)]
+        sampling launch, sampled ahead of the GCN on the sampler streams.  ``next_pairs``:
+        iterations of the next call, whose first plan groups are sampled ahead now."""
+        A = self.ahead
 
-        def compute(g, b):
-            for ci, (e, it) in enumerate(groups[g]):
+        def chunk(ps):
+            ps = [tuple(p) for p in ps]
+            return [tuple(ps[g0:g0 + A]) for g0 in range(0, len(ps), A)]
+
+        def compute(grp, b):
+            for ci, (e, it) in enumerate(grp):
                 self.compute(e, it, ci, b)
                 self.reduce_and_step()
                 if on_iteration is not None:
                     on_iteration(e, it)
 
-        self.pipeline(len(groups), lambda g, b: self.sample_group(groups[g], b), compute)
+        self.pipeline(chunk(pairs), lambda grp, b: self.sample_group(list(grp), b), compute,
+                      next_groups=chunk(next_pairs))
 
-    def check_errors(self):
+    def check_errors(self, clear: bool = False):
+        """Raise the reference's exception for any error of a plan consumed so far
+        (sticky per arena, so a later sampling call cannot hide it), or of a plan still
+        sampled ahead."""
         torch = _torch()
         torch.cuda.synchronize()
+        for ps, _ in self.bufs:
+            check(lib.skg_plans_sticky_error(ps.h, 1 if clear else 0))
         for ps, _ in self.bufs:
             for i in range(ps.n_slots):
                 _, info, rc = ps.stats(i)
@@ -823,6 +863,7 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
         if it != tr.per_epoch - 1:
             return
         losses = tr.losses.cpu().numpy()
+        tr.check_errors()  # training.py:296-297 raises inside the epoch; here at its end
         ledger = tr.ledger[epoch]
         loss_sum = np.zeros(k)
         loss_cnt = np.zeros(k, dtype=np.int64)

@@ -55,11 +55,13 @@ def er_edges(n, p, seed):
 
 
 def ref_graph_from_shaped(sgph):
+    feats = sgph.features.astype(np.float64) if sgph.features.shape[1] else None
+    labels = sgph.labels if np.ndim(sgph.labels) == 1 else None  # multi-hot: no reference head
     return sg.WeightedGraph(n_nodes=sgph.n_nodes, offsets=sgph.offsets,
                             neighbors=sgph.neighbors.astype(np.int64),
                             weights=sgph.weights, normalized=True,
-                            features=sgph.features.astype(np.float64),
-                            labels=sgph.labels, train_mask=sgph.train_mask,
+                            features=feats,
+                            labels=labels, train_mask=sgph.train_mask,
                             val_mask=sgph.val_mask, test_mask=sgph.test_mask)
 
 
@@ -271,7 +273,8 @@ def small_cases(st: Store):
 def shaped_cases(st: Store, shapes):
     """Benchmark-shaped graphs from the O(m) generator, reference plans on top."""
     for shape, k, runs, sampler in shapes:
-        sgph = make_shaped_graph(shape, seed=0)
+        # plans never read features; the large shapes skip them (YouTube's would be 18 GB)
+        sgph = make_shaped_graph(shape, seed=0, with_features=shape not in ("youtube", "amazon"))
         g = ref_graph_from_shaped(sgph)
         case_g = f"shape_{shape}"
         st.meta[case_g] = dict(kind="shape", shape=shape, seed=0,
@@ -316,8 +319,92 @@ def shaped_cases(st: Store, shapes):
                   flush=True)
 
 
+def reddit_fb_cases(st: Store):
+    """loss_and_backward / forward (training.py:261-318) at the benchmarked configuration:
+    Reddit-shaped graph, dims [602, 256, 256, 256, 256, 41], init_model seed 0, the synth
+    features, on the golden_reddit plans (skewed D=8 / full / local).  Gradients are
+    stored in full for the skewed plan (the bench's mode); for every plan a seeded sample
+    of 8192 entries per layer plus each layer's Frobenius norm."""
+    sgph = make_shaped_graph("reddit", seed=0)
+    g = ref_graph_from_shaped(sgph)
+    part = sg.partition_nodes(sgph.n_nodes, 8, "random", seed=1)
+    dims = [602, 256, 256, 256, 256, 41]
+    model = sg.init_model(dims, seed=0)
+    st.meta["shape_reddit"] = dict(kind="shape", shape="reddit", seed=0,
+                                   structure_sha=sgph.structure_hash(),
+                                   features_sha=sgph.features_hash())
+    for j, (mode, D, worker) in enumerate([("skewed", 8.0, 0), ("full", 0.0, 1), ("local", 0.0, 2)]):
+        cfg = sg.SamplerConfig(budget=512, mode=mode, skew_constant=D)
+        wt = np.flatnonzero(g.train_mask & (part.owner == worker))
+        batch = sg.node_set(sg.spawn_rng(0, "batch", 0, 0, worker).choice(
+            wt, size=min(512, len(wt)), replace=False))
+        plan = sg.ladies_plan(g, part, worker, batch, cfg, 5, sg.spawn_rng(0, "plan", 0, 0, worker))
+        loss, grads = sg.loss_and_backward(model, plan, g.features, g.labels)
+        logits = sg.forward(model, plan, g.features)
+        case = f"reddit_fb_{j:02d}"
+        st.meta[case] = dict(kind="reddit_fb", mode=mode, D=D, worker=worker, epoch=0, it=0,
+                             seed=0, k=8, pseed=1, budget=512, n_layers=5, dims=dims,
+                             model_seed=0, full_grads=j == 0)
+        st.put(case, "batch", plan.batch)
+        st.put(case, "remote", plan.remote_per_layer())
+        st.put(case, "loss", np.float64(loss))
+        st.put(case, "logits", logits)
+        sel = np.random.default_rng(1234)
+        for l, gr in enumerate(grads):
+            idx = sel.choice(gr.size, size=min(8192, gr.size), replace=False)
+            st.put(case, f"grad{l}_idx", idx.astype(np.int64))
+            st.put(case, f"grad{l}_val", gr.reshape(-1)[idx])
+            st.put(case, f"grad{l}_norm", np.float64(np.linalg.norm(gr)))
+            if j == 0:
+                st.put(case, f"grad{l}", gr)
+        print(case, loss, flush=True)
+
+
+def reddit_pipeline_cases(st: Store, iters=3, k=8):
+    """Every worker's plan of iterations (0, 0..iters-1) at the Reddit shape, k = 8,
+    skewed D = 8 (the bench's 24-plan look-ahead group), and the ledger they make
+    (training.py:486-499): the CUDA Trainer pipeline must reproduce them bit for bit."""
+    sgph = make_shaped_graph("reddit", seed=0, with_features=False)
+    g = sg.WeightedGraph(n_nodes=sgph.n_nodes, offsets=sgph.offsets,
+                         neighbors=sgph.neighbors.astype(np.int64), weights=sgph.weights,
+                         normalized=True, train_mask=sgph.train_mask)
+    part = sg.partition_nodes(sgph.n_nodes, k, "random", seed=1)
+    cfg = sg.SamplerConfig(budget=512, mode="skewed", skew_constant=8.0)
+    ledger = np.zeros((k, 5), dtype=np.int64)
+    st.meta["pipeline"] = dict(kind="pipeline", shape="reddit", k=k, pseed=1, mode="skewed",
+                               D=8.0, budget=512, batch_size=512, n_layers=5, seed=0,
+                               iters=iters, structure_sha=sgph.structure_hash())
+    for it in range(iters):
+        for w in range(k):
+            wt = np.flatnonzero(g.train_mask & (part.owner == w))
+            batch = sg.node_set(sg.spawn_rng(0, "batch", 0, it, w).choice(
+                wt, size=min(512, len(wt)), replace=False))
+            plan = sg.ladies_plan(g, part, w, batch, cfg, 5, sg.spawn_rng(0, "plan", 0, it, w))
+            ledger[w] += plan.remote_per_layer()
+            case = f"pipe_{it}_{w}"
+            st.put(case, "batch", plan.batch.astype(np.int32))
+            st.put(case, "remote", plan.remote_per_layer())
+            for l, L in enumerate(plan.layers):
+                b = L.block.tocsr()
+                st.put(case, f"L{l}/nodes", L.nodes.astype(np.int32))
+                st.put(case, f"L{l}/indptr", b.indptr.astype(np.int32))
+                st.put(case, f"L{l}/indices", b.indices.astype(np.int32))
+                st.put(case, f"L{l}/data", b.data)
+                st.put(case, f"L{l}/q_sha", np.array(sha(L.dist.q) if L.dist is not None else ""))
+            print(case, [len(L.nodes) for L in plan.layers], flush=True)
+    st.put("pipeline", "ledger", ledger)
+
+
 if __name__ == "__main__":
     which = sys.argv[1:] or ["small", "cora", "reddit_s", "amazon_s", "reddit"]
+    if "reddit_fb" in which:
+        st = Store()
+        reddit_fb_cases(st)
+        st.save(HERE / "golden_reddit_fb.npz")
+    if "pipeline" in which:
+        st = Store()
+        reddit_pipeline_cases(st)
+        st.save(HERE / "golden_pipeline.npz")
     if "small" in which:
         st = Store()
         small_cases(st)
@@ -332,6 +419,11 @@ if __name__ == "__main__":
          "saint"),
         ("reddit", 8, [("skewed", 8.0, 0, 0, 0), ("full", 0.0, 0, 0, 1), ("local", 0.0, 0, 0, 2)],
          "ladies"),
+        # > 16 x 65536 nodes: the device takes the global-atomic expand path
+        ("youtube", 8, [("skewed", 8.0, 0, 0, 0), ("full", 0.0, 0, 1, 3), ("local", 0.0, 0, 2, 5)],
+         "ladies"),
+        # the full Amazon shape (1.6M nodes, 132M CSR entries), GraphSAINT subgraph 4500
+        ("amazon", 8, [("skewed", 8.0, 0, 0, 1)], "saint"),
     ]:
         if shape in which:
             st = Store()

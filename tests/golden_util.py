@@ -58,17 +58,22 @@ def small_graph(name):
 
 
 @functools.lru_cache(maxsize=4)
-def shaped(shape, device=None):
+def shaped(shape, device=None, with_features=None):
+    """The benchmark-shaped graph; plan-only checks of the large shapes skip the features
+    (YouTube's would be 9 GB)."""
     from paper_2101_07706_b200.synth import make_shaped_graph
-    sg = make_shaped_graph(shape, seed=0, device=device)
+    if with_features is None:
+        with_features = shape not in ("youtube", "amazon")
+    sg = make_shaped_graph(shape, seed=0, device=device, with_features=with_features)
     return sg
 
 
 def oracle_graph_from_shaped(sgph):
     return O.Graph(n_nodes=sgph.n_nodes, offsets=sgph.offsets,
                    neighbors=sgph.neighbors.astype(np.int64), weights=sgph.weights,
-                   normalized=True, features=sgph.features.astype(np.float64),
-                   labels=sgph.labels, train_mask=sgph.train_mask, val_mask=sgph.val_mask,
+                   normalized=True,
+                   features=sgph.features.astype(np.float64) if sgph.features.shape[1] else None,
+                   labels=sgph.labels if np.ndim(sgph.labels) == 1 else None, train_mask=sgph.train_mask, val_mask=sgph.val_mask,
                    test_mask=sgph.test_mask)
 
 

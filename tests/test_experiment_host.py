@@ -93,3 +93,14 @@ def test_partition_csv(tmp_path):
     p.write_text("0,1\n2,1\n")
     with pytest.raises(ValueError, match="misses nodes"):
         P.load_partition_csv(p, 3, 2)
+
+
+def test_partition_csv_errors_in_file_order(tmp_path):
+    """partition.py:77-98: rows are checked as they are read; the message carries the line."""
+    p = tmp_path / "p.csv"
+    p.write_text("node,worker\n0,1\n7,0\nbad\n")
+    with pytest.raises(ValueError, match=r"p\.csv:3: node 7 out of range"):
+        P.load_partition_csv(p, 3, 2)
+    p.write_text("0,1\n1,5\n")
+    with pytest.raises(ValueError, match=r"p\.csv:2: worker 5 out of range"):
+        P.load_partition_csv(p, 3, 2)

@@ -167,8 +167,10 @@ def _shaped_pkg(shape):
     return sgph, P().from_shaped(sgph)
 
 
-@pytest.mark.parametrize("shape", ["cora", "reddit_s", "amazon_s", "reddit"])
+@pytest.mark.parametrize("shape", ["cora", "reddit_s", "amazon_s", "reddit", "youtube", "amazon"])
 def test_shaped_golden(shape):
+    """Reference plans at the benchmark shapes.  YouTube (1.1M nodes > 16 x 65536) runs the
+    global-atomic expand path; Amazon is the full 1.6M-node, 132M-entry GraphSAINT shape."""
     try:
         G2 = golden(shape)
     except FileNotFoundError:

@@ -77,7 +77,7 @@ def test_train_distributed_small(case):
         np.testing.assert_allclose(w, G.get(case, f"w{l}"), rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("shape", ["cora", "reddit_s", "amazon_s"])
+@pytest.mark.parametrize("shape", ["cora", "reddit_s", "amazon_s", "youtube", "amazon"])
 def test_shaped_plans(shape):
     G2 = golden(shape)
     gm = G2.meta[f"shape_{shape}"]
@@ -104,3 +104,57 @@ def test_shaped_plans(shape):
             plan = O.saint_plan(g, part, m["worker"], train, m["budget"], cfg, m["n_layers"], rng,
                                 norms=None if m["mode"] == "local" else saint_norms)
         assert_plan_equal(plan_to_dict(plan), G2.expected_plan(case))
+
+
+def test_reddit_forward_backward_golden():
+    """The oracle's loss_and_backward at the benchmarked configuration (Reddit shape, dims
+    [602, 256 x 4, 41]) against the reference's (tests/golden/golden_reddit_fb.npz)."""
+    G2 = golden("reddit_fb")
+    sgph = shaped("reddit")
+    assert sgph.structure_hash() == G2.meta["shape_reddit"]["structure_sha"]
+    assert sgph.features_hash() == G2.meta["shape_reddit"]["features_sha"]
+    g = oracle_graph_from_shaped(sgph)
+    part = O.partition_nodes(g.n_nodes, 8, "random", seed=1)
+    for case in G2.cases("reddit_fb"):
+        m = G2.meta[case]
+        batch = shaped_batch(g, part, m)
+        np.testing.assert_array_equal(batch, G2.get(case, "batch"))
+        plan = O.ladies_plan(g, part, m["worker"], batch,
+                             O.SamplerConfig(budget=512, skew_constant=m["D"], mode=m["mode"]), 5,
+                             O.spawn_rng(0, "plan", 0, 0, m["worker"]))
+        np.testing.assert_array_equal(plan.remote_per_layer(), G2.get(case, "remote"))
+        ws = O.init_model(m["dims"], m["model_seed"])
+        loss, grads = O.loss_and_backward(ws, plan, g.features, g.labels)
+        assert loss == pytest.approx(float(G2.get(case, "loss")), rel=1e-12)
+        np.testing.assert_allclose(O.forward(ws, plan, g.features), G2.get(case, "logits"),
+                                   rtol=1e-10, atol=1e-13)
+        for l, gr in enumerate(grads):
+            idx = G2.get(case, f"grad{l}_idx")
+            np.testing.assert_allclose(gr.reshape(-1)[idx], G2.get(case, f"grad{l}_val"),
+                                       rtol=1e-9, atol=1e-15)
+            assert np.linalg.norm(gr) == pytest.approx(float(G2.get(case, f"grad{l}_norm")), rel=1e-12)
+
+
+def test_reddit_pipeline_golden_plans():
+    """The oracle's plans for one 24-plan look-ahead group (iterations 0..2, k = 8) at the
+    Reddit shape equal the reference's (golden_pipeline.npz), a spot check of 4 plans."""
+    G2 = golden("pipeline")
+    m = G2.meta["pipeline"]
+    sgph = shaped("reddit")
+    assert sgph.structure_hash() == m["structure_sha"]
+    g = oracle_graph_from_shaped(sgph)
+    part = O.partition_nodes(g.n_nodes, m["k"], "random", seed=m["pseed"])
+    cfg = O.SamplerConfig(budget=m["budget"], skew_constant=m["D"], mode=m["mode"])
+    for it, w in ((0, 0), (1, 3), (2, 7), (2, 4)):
+        meta = dict(seed=0, epoch=0, it=it, worker=w, budget=m["batch_size"])
+        batch = shaped_batch(g, part, meta)
+        plan = O.ladies_plan(g, part, w, batch, cfg, 5, O.spawn_rng(0, "plan", 0, it, w))
+        case = f"pipe_{it}_{w}"
+        np.testing.assert_array_equal(plan.batch, G2.get(case, "batch"))
+        np.testing.assert_array_equal(plan.remote_per_layer(), G2.get(case, "remote"))
+        for l, L in enumerate(plan.layers):
+            b = L.block.tocsr()
+            np.testing.assert_array_equal(L.nodes, G2.get(case, f"L{l}/nodes"))
+            np.testing.assert_array_equal(b.indptr, G2.get(case, f"L{l}/indptr"))
+            np.testing.assert_array_equal(b.indices, G2.get(case, f"L{l}/indices"))
+            np.testing.assert_array_equal(b.data, G2.get(case, f"L{l}/data"))
