@@ -751,6 +751,24 @@ def kernel_table(lib, steps_fn, W, K, stats, tr, T, peaks, saint, budget):
     return out, all_ms
 
 
+def ncu_traffic(kernel_label):
+    """DRAM bytes per launch of the roofline kernel from the committed ncu --set full
+    extract (profiles/ncu_traffic.json, tools/ncu_traffic.py; cold-cache replay, so an upper
+    bound on the in-step traffic); null when the kernel was not captured."""
+    path = ROOT / "profiles" / "ncu_traffic.json"
+    base = kernel_label.split(" ")[0].split("<")[0]
+    try:
+        table = json.loads(path.read_text())
+    except (OSError, ValueError):
+        return {"traffic": None}
+    hits = [k for k in table if k == base or k.startswith(base + "_")]
+    if not hits:
+        return {"traffic": None}
+    t = table[hits[0]]
+    return {"traffic": int(t["dram_bytes"]), "traffic_source": f"profiles/ncu_traffic.json ({hits[0]}, "
+            f"mean of {t['launches']} ncu --set full launches, cold cache)"}
+
+
 # ---------------------------------------------------------------------------- CPU oracle
 def _oracle_setup(args, sg, saint_norms=None):
     """The oracle (a CPU restatement of the reference) on the same synthetic graph.

@@ -36,6 +36,27 @@ extern "C" {
 #define SKG_DT_F32 0
 #define SKG_DT_F64 1
 
+#define SKG_RNG_PCG64 0    /* numpy PCG64 (default_rng / spawn_rng, seeding.py:27) */
+#define SKG_RNG_PHILOX 1   /* numpy Philox (Philox4x64-10) */
+#define SKG_RNG_EXPLICIT 2 /* uniforms drawn by the caller's Generator (any bit generator) */
+
+/* The uniform stream of one plan: the `rng` argument of ladies_plan / saint_plan
+ * (training.py:162-164, 216-219), consumed by Generator.choice's random(B) at
+ * sampling.py:184.  Plan draws number d = 1, 2, ... in consumption order.
+ *   PCG64:    w[0..3] = state_hi, state_lo, inc_hi, inc_lo; draw d = output after d steps.
+ *   PHILOX:   w[0..3] = counter, w[4..5] = key, w[6..9] = buffer, buffer_pos in 0..4
+ *             (numpy's bit_generator.state); draw d = numpy's d-th next_uint64.
+ *   EXPLICIT: uniforms[d-1] (host memory, n_uniforms >= n_layers * budget covers every
+ *             draw a plan can make); the caller advances its Generator by the consumed
+ *             count (skg_plan_stats info[1]) afterwards. */
+typedef struct skg_rng {
+  int32_t kind;
+  int32_t buffer_pos;
+  uint64_t w[10];
+  const double* uniforms;
+  int64_t n_uniforms;
+} skg_rng;
+
 typedef struct skg_ctx skg_ctx;
 typedef struct skg_plans skg_plans;
 typedef struct skg_gcn skg_gcn;
@@ -123,6 +144,10 @@ int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* workers,
                              const int32_t* batch_len, uint64_t d_batch, int64_t batch_stride,
                              int mode, double skew_constant, double min_scale,
                              const uint64_t* rng_states, void* stream);
+/* skg_ladies_sample with one skg_rng per slot (PCG64, Philox or explicit uniforms). */
+int skg_ladies_sample_rng(skg_plans* ps, int n, const int32_t* workers, const int64_t* batch_off,
+                          const int64_t* batch_ids, int mode, double skew_constant,
+                          double min_scale, const skg_rng* rngs, void* stream);
 /* SAINT candidate set (sorted training nodes).  precompute != 0 caches
  * train_column_norms (training.py:211-213) used by full / skewed modes. */
 // column_norms(g, rows, candidates) for large row sets: pull formulation (ordered fold over
@@ -136,6 +161,10 @@ int skg_saint_set_candidates(skg_plans* ps, const int64_t* train_ids, int64_t n_
 int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, int mode,
                      double skew_constant, double min_scale, const uint64_t* rng_states,
                      void* stream);
+/* skg_saint_sample with one skg_rng per slot. */
+int skg_saint_sample_rng(skg_plans* ps, int n, const int32_t* workers, int mode,
+                         double skew_constant, double min_scale, const skg_rng* rngs,
+                         void* stream);
 /* CommLedger.add_plan (training.py:127-128) on device: ledger_dev is int64 [k x n_layers]
  * (one epoch); adds remote_per_layer of slots [slot0, slot0+n) to their workers' rows. */
 int skg_plans_ledger_add(skg_plans* ps, int slot0, int n, uint64_t ledger_dev, void* stream);

@@ -71,6 +71,18 @@ _sig("skg_plans_destroy", C.c_int, vp)
 _sig("skg_ladies_sample", C.c_int, vp, C.c_int, P(i32), P(i64), P(i64), C.c_int, dbl, dbl, P(u64), vp)
 _sig("skg_ladies_sample_device", C.c_int, vp, C.c_int, P(i32), P(i32), u64, i64, C.c_int, dbl, dbl,
      P(u64), vp)
+
+
+class SkgRng(C.Structure):
+    """skg_rng (include/skewgcn_b200.h): one plan's uniform stream."""
+    _fields_ = [("kind", C.c_int32), ("buffer_pos", C.c_int32), ("w", C.c_uint64 * 10),
+                ("uniforms", P(C.c_double)), ("n_uniforms", C.c_int64)]
+
+
+RNG_PCG64, RNG_PHILOX, RNG_EXPLICIT = 0, 1, 2
+_sig("skg_ladies_sample_rng", C.c_int, vp, C.c_int, P(i32), P(i64), P(i64), C.c_int, dbl, dbl,
+     P(SkgRng), vp)
+_sig("skg_saint_sample_rng", C.c_int, vp, C.c_int, P(i32), C.c_int, dbl, dbl, P(SkgRng), vp)
 _sig("skg_saint_set_candidates", C.c_int, vp, P(i64), i64, C.c_int, vp)
 _sig("skg_column_norms_pull", C.c_int, vp, P(i64), i64, P(i64), i64, P(C.c_double))
 _sig("skg_saint_sample", C.c_int, vp, C.c_int, P(i32), C.c_int, dbl, dbl, P(u64), vp)
@@ -99,7 +111,8 @@ EXPORTED = [
     "skg_spawn_pcg64", "skg_choice_noreplace", "skg_iteration_inputs", "skg_ctx_create",
     "skg_ctx_destroy", "skg_ctx_set_features", "skg_ctx_set_feature_map", "skg_ctx_feature_ptr", "skg_ctx_shard_upload",
     "skg_ctx_set_labels", "skg_ctx_set_multilabels", "skg_gcn_set_loss", "skg_ctx_set_owner", "skg_ctx_info", "skg_plans_ledger_add", "skg_plans_sticky_error", "skg_ipc_handle", "skg_ipc_open", "skg_ipc_close",
-    "skg_plans_create", "skg_plans_destroy", "skg_ladies_sample", "skg_ladies_sample_device", "skg_saint_set_candidates", "skg_column_norms_pull",
+    "skg_plans_create", "skg_plans_destroy", "skg_ladies_sample", "skg_ladies_sample_device",
+    "skg_ladies_sample_rng", "skg_saint_sample_rng", "skg_saint_set_candidates", "skg_column_norms_pull",
     "skg_saint_sample", "skg_plan_stats", "skg_plan_layer", "skg_gcn_create", "skg_gcn_destroy",
     "skg_gcn_step", "skg_gcn_step_batch", "skg_gcn_forward", "skg_gcn_read_logits", "skg_predict_logits",
     "skg_sgd_step", "skg_adam_step", "skg_zero", "skg_debug_reduce", "skg_debug_gemm", "skg_set_gemm_mode",

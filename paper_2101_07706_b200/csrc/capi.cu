@@ -247,6 +247,11 @@ struct skg_plans {
   // the last upload consumed by its stream before the host rewrites the staging
   PlanDev* h_pin = nullptr;
   int32_t* hb_pin = nullptr;
+  // explicit-uniform streams (SKG_RNG_EXPLICIT): n_slots x (L * budget) doubles, staged in
+  // pinned memory and uploaded with the descriptors
+  double* hu_pin = nullptr;
+  double* d_unif = nullptr;
+  size_t unif_staged = 0;
   cudaEvent_t up_ev = nullptr;
   bool up_armed = false;
 };
@@ -271,8 +276,59 @@ int upload_plans(skg_plans* ps, int n, size_t nb, cudaStream_t st) {
   std::memcpy(ps->h_pin, ps->h.data(), sizeof(PlanDev) * n);
   CK(cudaMemcpyAsync(ps->d_plans, ps->h_pin, sizeof(PlanDev) * n, cudaMemcpyHostToDevice, st));
   if (nb) CK(cudaMemcpyAsync(ps->d_batch, ps->hb_pin, sizeof(int32_t) * nb, cudaMemcpyHostToDevice, st));
+  if (ps->unif_staged) {
+    CK(cudaMemcpyAsync(ps->d_unif, ps->hu_pin, sizeof(double) * ps->unif_staged, cudaMemcpyHostToDevice, st));
+    ps->unif_staged = 0;
+  }
   CK(cudaEventRecord(ps->up_ev, st));
   ps->up_armed = true;
+  return SKG_OK;
+}
+
+// slot i's uniform stream: `rngs[i]`, or the PCG64 words pcg[4i..4i+3] (older entry points).
+// Explicit uniforms are staged for upload_plans (after staging_ready, so the pinned buffer
+// is free); their count is capped to the n_layers * budget draws a plan can make.
+int set_rng(skg_plans* ps, PlanDev& P, int i, const skg_rng* rngs, const uint64_t* pcg) {
+  P.rng_kind = RNG_PCG64;
+  P.rng_pos = 4;
+  P.uniforms = nullptr;
+  P.n_uniforms = 0;
+  if (!rngs) {
+    for (int q = 0; q < 4; ++q) P.rng[q] = pcg[4 * i + q];
+    return SKG_OK;
+  }
+  const skg_rng& r = rngs[i];
+  if (r.kind == SKG_RNG_PCG64) {
+    for (int q = 0; q < 4; ++q) P.rng[q] = r.w[q];
+  } else if (r.kind == SKG_RNG_PHILOX) {
+    if (r.buffer_pos < 0 || r.buffer_pos > 4) {
+      set_error("Philox buffer_pos out of range");
+      return SKG_ERR_ARG;
+    }
+    P.rng_kind = RNG_PHILOX;
+    P.rng_pos = r.buffer_pos;
+    for (int q = 0; q < 10; ++q) P.phx[q] = r.w[q];
+  } else if (r.kind == SKG_RNG_EXPLICIT) {
+    if (!r.uniforms || r.n_uniforms < 0) {
+      set_error("explicit uniform stream without uniforms");
+      return SKG_ERR_ARG;
+    }
+    const size_t per = (size_t)ps->L * (size_t)ps->budget;
+    if (!ps->hu_pin) {
+      CK(cudaHostAlloc(reinterpret_cast<void**>(&ps->hu_pin), sizeof(double) * per * ps->n_slots,
+                       cudaHostAllocDefault));
+      CK(cudaMalloc(&ps->d_unif, sizeof(double) * per * ps->n_slots));
+    }
+    const size_t cnt = std::min<size_t>((size_t)r.n_uniforms, per);
+    std::memcpy(ps->hu_pin + (size_t)i * per, r.uniforms, sizeof(double) * cnt);
+    ps->unif_staged = std::max(ps->unif_staged, (size_t)i * per + cnt);
+    P.rng_kind = RNG_EXPLICIT;
+    P.uniforms = ps->d_unif + (size_t)i * per;
+    P.n_uniforms = (int64_t)cnt;
+  } else {
+    set_error("unknown rng kind");
+    return SKG_ERR_ARG;
+  }
   return SKG_OK;
 }
 
@@ -909,6 +965,8 @@ extern "C" int skg_plans_destroy(skg_plans* ps) {
   }
   if (ps->h_pin) cudaFreeHost(ps->h_pin);
   if (ps->hb_pin) cudaFreeHost(ps->hb_pin);
+  if (ps->hu_pin) cudaFreeHost(ps->hu_pin);
+  cudaFree(ps->d_unif);
   cudaFree(ps->arena);
   cudaFree(ps->d_scal);
   cudaFree(ps->d_plans);
@@ -938,9 +996,9 @@ static int status_from_err(int err) {
   return SKG_OK;
 }
 
-extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
-                                 const int64_t* batch_off, const int64_t* batch_ids, int mode,
-                                 double D, double min_scale, const uint64_t* rng, void* stream) {
+static int ladies_sample(skg_plans* ps, int n, const int32_t* workers, const int64_t* batch_off,
+                         const int64_t* batch_ids, int mode, double D, double min_scale,
+                         const skg_rng* rngs, const uint64_t* rng, void* stream) {
   ARG(ps && ps->kind == KIND_LADIES, "not a LADIES plan set");
   ARG(n >= 1 && n <= ps->n_slots, "slot count out of range");
   ARG(mode >= 0 && mode <= 2, "unknown mode");
@@ -975,7 +1033,8 @@ extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
     P.mode = mode;
     P.D = D;
     P.min_scale = min_scale;
-    for (int q = 0; q < 4; ++q) P.rng[q] = rng[4 * i + q];
+    rc = set_rng(ps, P, i, rngs, rng);
+    if (rc) return rc;
     P.batch_len = (int32_t)len;
     P.batch = ps->d_batch + (size_t)i * ps->cap_batch;
     P.cand_norm = nullptr;
@@ -986,6 +1045,20 @@ extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
   const int max_upper = ps->L > 1 ? std::max<int>(ps->cap_batch, (int)std::min<int64_t>(ps->budget, ps->cap_cand))
                                   : ps->cap_batch;
   return run_ladies(ps, n, max_upper, st);
+}
+
+extern "C" int skg_ladies_sample(skg_plans* ps, int n, const int32_t* workers,
+                                 const int64_t* batch_off, const int64_t* batch_ids, int mode,
+                                 double D, double min_scale, const uint64_t* rng, void* stream) {
+  ARG(rng, "bad arguments");
+  return ladies_sample(ps, n, workers, batch_off, batch_ids, mode, D, min_scale, nullptr, rng, stream);
+}
+
+extern "C" int skg_ladies_sample_rng(skg_plans* ps, int n, const int32_t* workers,
+                                     const int64_t* batch_off, const int64_t* batch_ids, int mode,
+                                     double D, double min_scale, const skg_rng* rngs, void* stream) {
+  ARG(rngs, "bad arguments");
+  return ladies_sample(ps, n, workers, batch_off, batch_ids, mode, D, min_scale, rngs, nullptr, stream);
 }
 
 extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* workers,
@@ -1011,7 +1084,8 @@ extern "C" int skg_ladies_sample_device(skg_plans* ps, int n, const int32_t* wor
     P.mode = mode;
     P.D = D;
     P.min_scale = min_scale;
-    for (int q = 0; q < 4; ++q) P.rng[q] = rng[4 * i + q];
+    rc = set_rng(ps, P, i, nullptr, rng);
+    if (rc) return rc;
     P.batch_len = batch_len[i];
     P.batch = reinterpret_cast<const int32_t*>(d_batch) + (size_t)i * batch_stride;
     P.cand_norm = nullptr;
@@ -1138,14 +1212,18 @@ extern "C" int skg_saint_set_candidates(skg_plans* ps, const int64_t* train, int
   return status_from_err(err);
 }
 
-extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, int mode, double D,
-                                double min_scale, const uint64_t* rng, void* stream) {
+static int saint_sample(skg_plans* ps, int n, const int32_t* workers, int mode, double D,
+                        double min_scale, const skg_rng* rngs, const uint64_t* rng, void* stream) {
   ARG(ps && ps->kind == KIND_SAINT, "not a SAINT plan set");
   ARG(ps->d_train, "call skg_saint_set_candidates first");
   ARG(n >= 1 && n <= ps->n_slots, "slot count out of range");
   skg_ctx* c = ps->ctx;
   CK(cudaSetDevice(c->device));
   cudaStream_t st = (cudaStream_t)stream;
+  {
+    const int urc = staging_ready(ps);  // the pinned staging (uniforms) is free again
+    if (urc) return urc;
+  }
   CK(cudaMemsetAsync(ps->d_scal, 0, ps->scal_bytes, st));
   for (int i = 0; i < n; ++i) {
     const int w = workers[i];
@@ -1155,7 +1233,8 @@ extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, in
     P.mode = mode;
     P.D = D;
     P.min_scale = min_scale;
-    for (int q = 0; q < 4; ++q) P.rng[q] = rng[4 * i + q];
+    int rc = set_rng(ps, P, i, rngs, rng);
+    if (rc) return rc;
     if (mode == MODE_LOCAL) {
       if (ps->n_local[w] == 0) {
         set_error("no local training nodes to sample a subgraph from");
@@ -1185,13 +1264,23 @@ extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, in
     }
   }
   {
-    const int urc = staging_ready(ps);
-    if (urc) return urc;
     const int prc = upload_plans(ps, n, 0, st);
     if (prc) return prc;
   }
   return launch_saint(c->gdev(), ps->d_plans, n, ps->cap_rows, ps->cap_cand, ps->cap_pairs,
                       (int)ps->budget, st);
+}
+
+extern "C" int skg_saint_sample(skg_plans* ps, int n, const int32_t* workers, int mode, double D,
+                                double min_scale, const uint64_t* rng, void* stream) {
+  ARG(rng, "bad arguments");
+  return saint_sample(ps, n, workers, mode, D, min_scale, nullptr, rng, stream);
+}
+
+extern "C" int skg_saint_sample_rng(skg_plans* ps, int n, const int32_t* workers, int mode, double D,
+                                    double min_scale, const skg_rng* rngs, void* stream) {
+  ARG(rngs, "bad arguments");
+  return saint_sample(ps, n, workers, mode, D, min_scale, rngs, nullptr, stream);
 }
 
 __global__ void k_ledger_add(const PlanDev* plans, int L, int64_t* ledger, int32_t* sticky) {

@@ -7,6 +7,8 @@ namespace skg {
 
 enum Mode : int32_t { MODE_FULL = 0, MODE_LOCAL = 1, MODE_SKEWED = 2 };
 enum Kind : int32_t { KIND_LADIES = 0, KIND_SAINT = 1 };
+// uniform streams a plan's draws come from (the rng argument of training.py:162-164, 216-219)
+enum RngKind : int32_t { RNG_PCG64 = 0, RNG_PHILOX = 1, RNG_EXPLICIT = 2 };
 
 // Replicated topology (int32 columns, fp64 weights as stored by the reference's
 // WeightedGraph, graph.py:28-31) plus the ownership map (partition.py:21).
@@ -53,6 +55,11 @@ struct PlanDev {
   int64_t budget;
   double D, min_scale;
   uint64_t rng[4];          // PCG64 state (hi, lo) and increment (hi, lo)
+  int32_t rng_kind;         // RNG_PCG64 (rng), RNG_PHILOX (phx, rng_pos), RNG_EXPLICIT (uniforms)
+  int32_t rng_pos;          // Philox: numpy's buffer_pos (4 = buffer exhausted)
+  uint64_t phx[10];         // Philox4x64-10: counter[4], key[2], buffer[4] (numpy's state)
+  const double* uniforms;   // explicit: uniforms[d - 1] is the plan's d-th uniform
+  int64_t n_uniforms;
   int32_t batch_len;        // LADIES: |batch|; SAINT: |candidates|
   int32_t pad0;
   const int32_t* batch;     // LADIES batch ids; SAINT candidate ids (sorted)

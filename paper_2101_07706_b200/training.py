@@ -25,7 +25,8 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _device as D
-from ._native import DT, KIND_LADIES, KIND_SAINT, MODES, check, lib, ptr
+from ._native import (DT, KIND_LADIES, KIND_SAINT, MODES, RNG_EXPLICIT, RNG_PCG64, RNG_PHILOX, SkgRng,
+                      check, lib, ptr)
 from .graph import WeightedGraph, check_node_set, node_set
 from .partition import Partition
 from .sampling import ProbDist, SamplerConfig
@@ -173,10 +174,48 @@ class SamplePlan:
 
 
 def _uniform_source(rng, budget: int, n_layers: int):
+    """The plan's uniform stream (skg_rng) for any numpy Generator, which the reference
+    passes to Generator.choice (sampling.py:184).  PCG64 and Philox streams are generated
+    on the device from the bit generator's state; any other bit generator's uniforms are
+    drawn here from a copy of ``rng`` (n_layers * budget of them, every draw a plan can
+    make) and passed explicitly."""
+    if not isinstance(rng, np.random.Generator):
+        raise TypeError("rng must be a numpy.random.Generator")
+    r = SkgRng()
     gs = generator_state(rng)
-    if gs is None:
-        raise TypeError("the device sampler consumes PCG64 streams (numpy default_rng / spawn_rng)")
-    return gs[0]
+    if gs is not None:
+        r.kind = RNG_PCG64
+        for q in range(4):
+            r.w[q] = int(gs[0][q])
+        return r, None
+    st = rng.bit_generator.state
+    if st.get("bit_generator") == "Philox":
+        r.kind = RNG_PHILOX
+        words = list(st["state"]["counter"]) + list(st["state"]["key"]) + list(st["buffer"])
+        for q, v in enumerate(words):
+            r.w[q] = int(v)
+        r.buffer_pos = int(st["buffer_pos"])
+        return r, None
+    shadow = np.random.Generator(type(rng.bit_generator)())
+    shadow.bit_generator.state = st
+    u = np.ascontiguousarray(shadow.random(n_layers * budget), dtype=np.float64)
+    r.kind = RNG_EXPLICIT
+    r.uniforms = u.ctypes.data_as(C.POINTER(C.c_double))
+    r.n_uniforms = len(u)
+    return r, u
+
+
+def _advance(rng, n_draws: int) -> None:
+    """Leave ``rng`` where the reference's random(B) calls would (n_draws uniforms)."""
+    if n_draws <= 0:
+        return
+    name = rng.bit_generator.state.get("bit_generator")
+    if name == "PCG64":
+        advance_generator(rng, n_draws)
+    elif name == "Philox":
+        rng.bit_generator.random_raw(n_draws)  # next_uint64 per uniform; uint32 buffer kept
+    else:
+        rng.random(n_draws)
 
 
 def ladies_plan(g: WeightedGraph, partition: Partition, worker: int, batch, cfg: SamplerConfig,
@@ -191,16 +230,16 @@ def ladies_plan(g: WeightedGraph, partition: Partition, worker: int, batch, cfg:
         raise ValueError("worker id out of range")
     dg = D.device_graph(g)
     dg.ensure_owner(partition)
-    state = _uniform_source(rng, cfg.budget, n_layers)
+    src, _keep = _uniform_source(rng, int(cfg.budget), n_layers)
     ps = dg.acquire(KIND_LADIES, 1, n_layers, int(cfg.budget), int(len(batch)))
     lease = D.Lease(dg, ps, 0)
     off = np.array([0, len(batch)], dtype=np.int64)
     w = np.array([worker], dtype=np.int32)
-    check(lib.skg_ladies_sample(ps.h, 1, ptr(w, C.c_int32), ptr(off, C.c_int64), ptr(batch, C.c_int64),
-                                MODES[cfg.mode], float(cfg.skew_constant), float(cfg.min_scale),
-                                ptr(state, C.c_uint64), None))
+    check(lib.skg_ladies_sample_rng(ps.h, 1, ptr(w, C.c_int32), ptr(off, C.c_int64),
+                                    ptr(batch, C.c_int64), MODES[cfg.mode], float(cfg.skew_constant),
+                                    float(cfg.min_scale), C.byref(src), None))
     plan = SamplePlan(lease, batch, n_layers, KIND_LADIES)
-    advance_generator(rng, plan.draws_consumed)
+    _advance(rng, plan.draws_consumed)
     return plan
 
 
@@ -238,16 +277,17 @@ def saint_plan(g: WeightedGraph, partition: Partition, worker: int, train_nodes,
         raise ValueError("worker id out of range")
     dg = D.device_graph(g)
     dg.ensure_owner(partition)
-    state = _uniform_source(rng, subgraph_size, n_layers)
+    src, _keep = _uniform_source(rng, int(subgraph_size), n_layers)
     ps = dg.acquire(KIND_SAINT, 1, n_layers, int(subgraph_size), 1)
     lease = D.Lease(dg, ps, 0)
     _saint_set(dg, ps, train_nodes, cfg.mode != "local")
     w = np.array([worker], dtype=np.int32)
-    check(lib.skg_saint_sample(ps.h, 1, ptr(w, C.c_int32), MODES[cfg.mode], float(cfg.skew_constant),
-                               float(cfg.min_scale), ptr(state, C.c_uint64), None))
+    check(lib.skg_saint_sample_rng(ps.h, 1, ptr(w, C.c_int32), MODES[cfg.mode],
+                                   float(cfg.skew_constant), float(cfg.min_scale), C.byref(src),
+                                   None))
     plan = SamplePlan(lease, None, n_layers, KIND_SAINT)
     plan.batch = plan.layers[0].nodes
-    advance_generator(rng, plan.draws_consumed)
+    _advance(rng, plan.draws_consumed)
     return plan
 
 

@@ -66,8 +66,19 @@ def ref_graph_from_shaped(sgph):
 
 
 def make_rng(spec):
+    """("default", seed) | ("spawn", seed, *labels) | ("philox", key, skip) |
+    ("mt19937", seed) | ("sfc64", seed); `skip` next_uint64 outputs are consumed first so
+    the Philox buffer is part-used (buffer_pos != 4)."""
     if spec[0] == "default":
         return np.random.default_rng(spec[1])
+    if spec[0] == "philox":
+        g = np.random.Generator(np.random.Philox(key=spec[1]))
+        g.bit_generator.random_raw(spec[2])
+        return g
+    if spec[0] == "mt19937":
+        return np.random.Generator(np.random.MT19937(spec[1]))
+    if spec[0] == "sfc64":
+        return np.random.Generator(np.random.SFC64(spec[1]))
     return sg.spawn_rng(spec[1], *spec[2:])
 
 
@@ -319,6 +330,48 @@ def shaped_cases(st: Store, shapes):
                   flush=True)
 
 
+def rng_cases(st: Store):
+    """Plans driven by non-PCG64 Generators (the reference accepts any numpy Generator,
+    training.py:162-164, 216-219): Philox (fresh and with a part-used output buffer),
+    MT19937 and SFC64.  `after` = the next 4 random() values of the generator after the
+    plan, which pins how far the plan advanced it."""
+    n, e = 200, er_edges(200, 0.05, 5)
+    st.put("graph_er200", "edges", e)
+    st.put("graph_er200", "n", np.int64(n))
+    g = ref_graph_from_edges([tuple(x) for x in e.tolist()], n)
+    idx = 0
+    for kind, mode, D, rspec in [
+        ("ladies", "skewed", 8.0, ("philox", 12345, 0)),
+        ("ladies", "skewed", 8.0, ("philox", 7, 3)),
+        ("ladies", "full", 0.0, ("philox", 2**64 - 1, 1)),
+        ("ladies", "skewed", 4.0, ("mt19937", 3)),
+        ("ladies", "local", 0.0, ("sfc64", 9)),
+        ("saint", "skewed", 8.0, ("philox", 99, 2)),
+        ("saint", "full", 0.0, ("mt19937", 5)),
+    ]:
+        part = sg.partition_nodes(n, 4, "random", seed=9)
+        rng = make_rng(rspec)
+        if kind == "ladies":
+            batch = part.owned_by(2)[:40]
+            cfg = sg.SamplerConfig(budget=32, mode=mode, skew_constant=D)
+            plan = sg.ladies_plan(g, part, 2, batch, cfg, 5, rng)
+            meta = dict(kind="ladies", graph="er200", k=4, strategy="random", pseed=9, worker=2,
+                        batch=batch.tolist(), budget=32, mode=mode, D=D, min_scale=1.0,
+                        n_layers=5, rng=list(rspec))
+        else:
+            train = np.arange(0, n, 2)
+            cfg = sg.SamplerConfig(budget=8, mode=mode, skew_constant=D)
+            plan = sg.saint_plan(g, part, 1, train, 30, cfg, 3, rng)
+            meta = dict(kind="saint", graph="er200", k=4, strategy="random", pseed=9, worker=1,
+                        train=train.tolist(), size=30, budget=8, mode=mode, D=D, min_scale=1.0,
+                        n_layers=3, rng=list(rspec), precomputed=False)
+        case = f"rng_{idx:02d}"
+        st.meta[case] = meta
+        dump_plan(st, case, plan)
+        st.put(case, "after", rng.random(4))
+        idx += 1
+
+
 def reddit_fb_cases(st: Store):
     """loss_and_backward / forward (training.py:261-318) at the benchmarked configuration:
     Reddit-shaped graph, dims [602, 256, 256, 256, 256, 41], init_model seed 0, the synth
@@ -405,6 +458,10 @@ if __name__ == "__main__":
         st = Store()
         reddit_pipeline_cases(st)
         st.save(HERE / "golden_pipeline.npz")
+    if "rng" in which:
+        st = Store()
+        rng_cases(st)
+        st.save(HERE / "golden_rng.npz")
     if "small" in which:
         st = Store()
         small_cases(st)

@@ -84,8 +84,17 @@ def partition_for(meta, n):
 
 
 def make_rng(spec):
+    """Same construction as tests/golden/make_golden.py:make_rng."""
     if spec[0] == "default":
         return np.random.default_rng(spec[1])
+    if spec[0] == "philox":
+        g = np.random.Generator(np.random.Philox(key=spec[1]))
+        g.bit_generator.random_raw(spec[2])
+        return g
+    if spec[0] == "mt19937":
+        return np.random.Generator(np.random.MT19937(spec[1]))
+    if spec[0] == "sfc64":
+        return np.random.Generator(np.random.SFC64(spec[1]))
     return O.spawn_rng(spec[1], *spec[2:])
 
 

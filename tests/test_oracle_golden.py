@@ -158,3 +158,23 @@ def test_reddit_pipeline_golden_plans():
             np.testing.assert_array_equal(b.indptr, G2.get(case, f"L{l}/indptr"))
             np.testing.assert_array_equal(b.indices, G2.get(case, f"L{l}/indices"))
             np.testing.assert_array_equal(b.data, G2.get(case, f"L{l}/data"))
+
+
+GR = golden("rng")
+
+
+@pytest.mark.parametrize("case", GR.cases("ladies") + GR.cases("saint"))
+def test_non_pcg64_generators(case):
+    """Plans driven by Philox / MT19937 / SFC64 Generators (reference accepts any Generator)."""
+    m = GR.meta[case]
+    g = small_graph(m["graph"])
+    part = partition_for(m, g.n_nodes)
+    rng = make_rng(m["rng"])
+    if m["kind"] == "ladies":
+        plan = O.ladies_plan(g, part, m["worker"], np.array(m["batch"], dtype=np.int64),
+                             cfg_for(m), m["n_layers"], rng)
+    else:
+        plan = O.saint_plan(g, part, m["worker"], np.array(m["train"], dtype=np.int64), m["size"],
+                            cfg_for(m), m["n_layers"], rng)
+    assert_plan_equal(plan_to_dict(plan), GR.expected_plan(case))
+    np.testing.assert_array_equal(rng.random(4), GR.get(case, "after"))
