@@ -223,6 +223,7 @@ struct skg_plans {
   int64_t budget = 0, max_batch = 0;
   int cap_rows = 0, cap_cand = 0, cap_batch = 0;
   int64_t cap_pairs = 0;
+  int n_fr = 0;  // fused range expand: ranges per plan (0: the older expand kernels)
   std::vector<PlanDev> h;
   PlanDev* d_plans = nullptr;
   char* arena = nullptr;
@@ -337,7 +338,7 @@ int run_ladies(skg_plans* ps, int n, int max_upper, cudaStream_t st) {
   skg_ctx* c = ps->ctx;
   auto launch = [&](cudaStream_t s) {
     return launch_ladies(c->gdev(), ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
-                         (int)ps->budget, s);
+                         (int)ps->budget, ps->n_fr, s);
   };
   if (!graphs_on()) return launch(st);
   std::string key;
@@ -841,6 +842,15 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
   ps->cap_cand = (int)cap_cand;
   ps->cap_pairs = cap_pairs;
   ps->cap_batch = (int)cap_batch;
+  // fused range expand (sampler.cu k_lad_range): normalised graphs of <= kMaxFR ranges;
+  // SKG_EXPAND=ranges|global (or SKG_GLOBAL_EXPAND) selects the older expand kernels
+  {
+    const char* ex = getenv("SKG_EXPAND");
+    const bool off = getenv("SKG_GLOBAL_EXPAND") || (ex && std::string(ex) != "fused");
+    const int64_t nfr = (n + kFRange - 1) / kFRange;
+    ps->n_fr = (kind == KIND_LADIES && c->normalized && !off && nfr >= 1 && nfr <= kMaxFR &&
+                cap_rows <= kFusedMaxRows) ? (int)nfr : 0;
+  }
   const int Ls = kind == KIND_LADIES ? L : 1;
   int pw = 0;
   while (cap_cand > (112LL << pw)) ++pw;
@@ -854,11 +864,13 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
   Carver scal;
   std::vector<int32_t*> errs(n_slots), starv(n_slots), ctrs(n_slots);
   std::vector<int64_t*> draws(n_slots);
+  std::vector<unsigned long long*> looks(n_slots);
   for (int s = 0; s < n_slots; ++s) {
     scal.add(errs[s], 1);
     scal.add(starv[s], 1);
     scal.add(ctrs[s], 8);
     scal.add(draws[s], 1);
+    scal.add(looks[s], ps->n_fr ? (size_t)L * kMaxFR : 1);
   }
   ps->scal_bytes = scal.off;
   Carver cv;
@@ -874,9 +886,11 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     P.cap_tiles = cap_tiles;
     cv.add(P.bitmap, n_words);
     cv.add(P.sbitmap, n_words);
-    cv.add(P.cnt_pack, (size_t)(n / 2 + 1));
+    cv.add(P.cnt_pack, ps->n_fr ? 1 : (size_t)(n / 2 + 1));
     const bool lad = kind == KIND_LADIES, stw = lad && !c->normalized;
-    cv.add(P.slots, lad ? (size_t)std::max<int64_t>(n, 1) * kSlots : 4);
+    cv.add(P.slots, lad && !ps->n_fr ? (size_t)std::max<int64_t>(n, 1) * kSlots : 4);
+    cv.add(P.cslots, lad && c->normalized ? cap_cand : 1);
+    cv.add(P.rbounds, ps->n_fr ? (size_t)cap_rows * (ps->n_fr + 1) : 1);
     cv.add(P.slotw, stw ? (size_t)std::max<int64_t>(n, 1) * kSlots : 1);
     cv.add(P.ov, lad ? cap_pairs : 1);
     cv.add(P.ovw, stw ? cap_pairs : 1);
@@ -942,6 +956,8 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     P.starvation = starv[s];
     P.counters = ctrs[s];
     P.draws_consumed = draws[s];
+    P.look = looks[s];
+    P.n_fr = ps->n_fr;
     P.kind = kind;
     P.n_layers = L;
     P.budget = budget;

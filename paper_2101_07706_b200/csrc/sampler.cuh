@@ -76,6 +76,17 @@ struct PlanDev {
   // LADIES contributions (upper-row rank r of every pair (r, j)), by node: the first
   // kSlots arrivals in slots[j], later ones in the overflow list; candidates with more
   // than kSlots get a contiguous, row-sorted range hbuf[hoff[h] .. + count)
+  // normalised graphs: the contributions' row ranks by candidate rank k (4 x 16 bits):
+  // row-sorted for candidates with <= kSlots contributions, the first kSlots arrivals
+  // (any order) for heavier ones
+  uint2* cslots;            // [cap_cand]
+  // fused range expand (n_fr > 0): per upper row, the start of each kFRange-node column
+  // range in its CSR row (n_fr + 1 entries, the last = row end); look-back words of the
+  // range CTAs per layer (in the per-call zeroed scalars)
+  int32_t n_fr;
+  int32_t pad1;
+  int64_t* rbounds;         // [cap_rows * (n_fr + 1)]
+  unsigned long long* look; // [L * kMaxFR]
   uint16_t* slots;          // [n*kSlots]
   double* slotw;            // [n*kSlots] stored w_ij (graphs that are not normalised)
   int2* ov;                 // [cap_pairs] overflow pairs (j, r)
@@ -128,6 +139,10 @@ struct PlanDev {
 };
 
 constexpr int kSlots = 4;         // contributions kept per node before overflowing
+constexpr int kFRangeShift = 14;  // fused range expand: 16K nodes per range CTA
+constexpr int kFRange = 1 << kFRangeShift;
+constexpr int kMaxFR = 32;        // at most this many ranges (graphs up to 512K nodes)
+constexpr int kFusedMaxRows = 8192;  // upper rows per plan on the fused path
 constexpr int kRangeNodes = 65536;  // nodes per CTA of the shared-memory-counting expand
 constexpr int kMaxRanges = 16;      // beyond this many ranges per plan: global-atomic expand
 constexpr int kTileWords = 256;    // bitmap words per compaction tile (8 warps x 32 words)
@@ -139,7 +154,7 @@ constexpr int kPwSub = 256;        // pairwise-tree slots combined per CTA
 
 // Host-side launch of the full sampling pipeline for n_plans slots.
 int launch_ladies(const GraphDev& g, PlanDev* d_plans, int n_plans, int n_layers, int max_upper,
-                  int cap_cand, int64_t cap_pairs, int budget_max, cudaStream_t st);
+                  int cap_cand, int64_t cap_pairs, int budget_max, int n_fr, cudaStream_t st);
 int launch_saint(const GraphDev& g, PlanDev* d_plans, int n_plans, int cap_rows, int cap_cand,
                  int64_t cap_pairs, int budget_max, cudaStream_t st);
 int launch_pull_norms(const GraphDev& g, const int32_t* cand, int32_t n_cand,
