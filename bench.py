@@ -279,6 +279,8 @@ def kernel_bytes_8d(stats, budget):
     Z = sum(int(r[3]) for st in stats for r in st)
     B = sum(budget for st in stats for r in st if int(r[5]))
     return {"k_lad_expand_ranges": 8 * E + 12 * U, "k_lad_expand": 8 * E + 12 * U,
+            # the fused range kernel does the expansion, compaction and fold shares
+            "k_lad_range": 8 * E + 12 * U + 9 * N,
             "k_bitmap_compact": 1 * N, "k_lad_fold": 8 * N, "k_pw_leaves": 8 * N,
             "k_cs_maps": 8 * N, "k_draw_dedup": 8 * B + 12 * S, "k_lad_finish": 12 * Z}
 
