@@ -171,6 +171,8 @@ struct skg_ctx {
   bool symmetric = true;
   bool normalized = false;
   double* d_degd = nullptr;
+  int32_t* d_rstart = nullptr;  // fused range expand table (normalised graphs, n_fr ranges)
+  int32_t n_fr = 0;
   std::vector<int64_t> deg_desc_prefix;  // prefix sums of degrees sorted descending
   void* d_x = nullptr;
   int64_t F = 0, ldx = 0, x_rows = 0;
@@ -199,6 +201,8 @@ struct skg_ctx {
     g.n_words = (int32_t)((n + 31) / 32);
     g.normalized = normalized ? 1 : 0;
     g.degd = d_degd;
+    g.rstart = d_rstart;
+    g.n_fr = n_fr;
     return g;
   }
   FeatStore fstore() const {
@@ -605,6 +609,16 @@ extern "C" int skg_ctx_create(int device, int64_t n, int64_t nnz, const int64_t*
   c->normalized = (n > 0) && !bad;
   if (getenv("SKG_STORED_WEIGHTS")) c->normalized = false;  // experiment: read w, never recompute
   cudaFree(d_bad);
+  {  // graph-static range starts of the fused range expand (sampler.cu k_lad_range)
+    const int64_t nfr = (n + kFRange - 1) / kFRange;
+    if (c->normalized && nfr >= 1 && nfr <= kMaxFR) {
+      CK(cudaMalloc(&c->d_rstart, sizeof(int32_t) * (size_t)n * (nfr + 1)));
+      c->n_fr = (int32_t)nfr;
+      int rc = launch_build_rstart(c->gdev(), c->d_rstart, c->n_fr);
+      if (rc) return rc;
+      CK(cudaDeviceSynchronize());
+    }
+  }
   if (!c->symmetric) {  // host counting sort by column (rows ascending within a column)
     std::vector<int64_t> toff(n + 1, 0);
     for (int64_t e = 0; e < nnz; ++e) toff[neighbors[e] + 1]++;
@@ -641,6 +655,7 @@ extern "C" int skg_ctx_destroy(skg_ctx* c) {
   cudaFree(c->d_trow);
   cudaFree(c->d_tw);
   cudaFree(c->d_degd);
+  cudaFree(c->d_rstart);
   cudaFree(c->d_x);
   cudaFree(c->d_labels);
   cudaFree(c->d_ymulti);
@@ -847,9 +862,7 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
   {
     const char* ex = getenv("SKG_EXPAND");
     const bool off = getenv("SKG_GLOBAL_EXPAND") || (ex && std::string(ex) != "fused");
-    const int64_t nfr = (n + kFRange - 1) / kFRange;
-    ps->n_fr = (kind == KIND_LADIES && c->normalized && !off && nfr >= 1 && nfr <= kMaxFR &&
-                cap_rows <= kFusedMaxRows) ? (int)nfr : 0;
+    ps->n_fr = (kind == KIND_LADIES && c->n_fr > 0 && !off && cap_rows <= kFusedMaxRows) ? c->n_fr : 0;
   }
   const int Ls = kind == KIND_LADIES ? L : 1;
   int pw = 0;
@@ -890,7 +903,6 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     const bool lad = kind == KIND_LADIES, stw = lad && !c->normalized;
     cv.add(P.slots, lad && !ps->n_fr ? (size_t)std::max<int64_t>(n, 1) * kSlots : 4);
     cv.add(P.cslots, lad && c->normalized ? cap_cand : 1);
-    cv.add(P.rbounds, ps->n_fr ? (size_t)cap_rows * (ps->n_fr + 1) : 1);
     cv.add(P.slotw, stw ? (size_t)std::max<int64_t>(n, 1) * kSlots : 1);
     cv.add(P.ov, lad ? cap_pairs : 1);
     cv.add(P.ovw, stw ? cap_pairs : 1);

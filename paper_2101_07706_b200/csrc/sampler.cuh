@@ -25,6 +25,11 @@ struct GraphDev {
   int32_t n_words;       // ceil(n/32)
   int32_t normalized;    // every w_ij == 1/sqrt(d_i d_j) (graph.py:182), checked at load
   const double* degd;    // [n] row lengths as double (normalized graphs)
+  // fused range expand: rstart[i * (n_fr + 1) + q] = offset in row i of its first column
+  // >= q * kFRange (q = n_fr: the row length); graph-static, built at load
+  const int32_t* rstart;
+  int32_t n_fr;
+  int32_t pad_;
 };
 
 // Per-layer scalars of one plan.  Layers are indexed top-down while sampling
@@ -80,12 +85,10 @@ struct PlanDev {
   // row-sorted for candidates with <= kSlots contributions, the first kSlots arrivals
   // (any order) for heavier ones
   uint2* cslots;            // [cap_cand]
-  // fused range expand (n_fr > 0): per upper row, the start of each kFRange-node column
-  // range in its CSR row (n_fr + 1 entries, the last = row end); look-back words of the
-  // range CTAs per layer (in the per-call zeroed scalars)
+  // fused range expand (n_fr > 0, GraphDev.rstart): look-back words of the range CTAs per
+  // layer (in the per-call zeroed scalars)
   int32_t n_fr;
   int32_t pad1;
-  int64_t* rbounds;         // [cap_rows * (n_fr + 1)]
   unsigned long long* look; // [L * kMaxFR]
   uint16_t* slots;          // [n*kSlots]
   double* slotw;            // [n*kSlots] stored w_ij (graphs that are not normalised)
@@ -159,6 +162,8 @@ int launch_saint(const GraphDev& g, PlanDev* d_plans, int n_plans, int cap_rows,
                  int64_t cap_pairs, int budget_max, cudaStream_t st);
 int launch_pull_norms(const GraphDev& g, const int32_t* cand, int32_t n_cand,
                       const uint32_t* row_bitmap, double* out, int32_t* err, cudaStream_t st);
+// GraphDev.rstart for a graph of n_fr ranges (stream 0, synchronous use at load)
+int launch_build_rstart(const GraphDev& g, int32_t* rstart, int n_fr);
 void launch_set_bitmap(const int32_t* ids, int32_t n, uint32_t* bitmap, int32_t n_words,
                        cudaStream_t st);
 extern unsigned long long g_kernel_launches;
