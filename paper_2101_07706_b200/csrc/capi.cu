@@ -171,8 +171,9 @@ struct skg_ctx {
   bool symmetric = true;
   bool normalized = false;
   double* d_degd = nullptr;
-  int32_t* d_rstart = nullptr;  // fused range expand table (normalised graphs, n_fr ranges)
-  int32_t n_fr = 0;
+  // fused range expand tables (normalised graphs), one per range size, built on first use
+  bool fr_ok = false;
+  std::unordered_map<int, int32_t*> rstarts;
   std::vector<int64_t> deg_desc_prefix;  // prefix sums of degrees sorted descending
   void* d_x = nullptr;
   int64_t F = 0, ldx = 0, x_rows = 0;
@@ -201,8 +202,9 @@ struct skg_ctx {
     g.n_words = (int32_t)((n + 31) / 32);
     g.normalized = normalized ? 1 : 0;
     g.degd = d_degd;
-    g.rstart = d_rstart;
-    g.n_fr = n_fr;
+    g.rstart = nullptr;  // per plan set (skg_plans::rstart)
+    g.n_fr = 0;
+    g.fr_size = 0;
     return g;
   }
   FeatStore fstore() const {
@@ -228,6 +230,8 @@ struct skg_plans {
   int cap_rows = 0, cap_cand = 0, cap_batch = 0;
   int64_t cap_pairs = 0;
   int n_fr = 0;  // fused range expand: ranges per plan (0: the older expand kernels)
+  int fr_size = 0;  // nodes per range
+  const int32_t* rstart = nullptr;  // the context's table for fr_size
   std::vector<PlanDev> h;
   PlanDev* d_plans = nullptr;
   char* arena = nullptr;
@@ -341,7 +345,11 @@ int set_rng(skg_plans* ps, PlanDev& P, int i, const skg_rng* rngs, const uint64_
 int run_ladies(skg_plans* ps, int n, int max_upper, cudaStream_t st) {
   skg_ctx* c = ps->ctx;
   auto launch = [&](cudaStream_t s) {
-    return launch_ladies(c->gdev(), ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
+    GraphDev g = c->gdev();
+    g.rstart = ps->rstart;
+    g.n_fr = ps->n_fr;
+    g.fr_size = ps->fr_size;
+    return launch_ladies(g, ps->d_plans, n, ps->L, max_upper, ps->cap_cand, ps->cap_pairs,
                          (int)ps->budget, ps->n_fr, s);
   };
   if (!graphs_on()) return launch(st);
@@ -609,16 +617,9 @@ extern "C" int skg_ctx_create(int device, int64_t n, int64_t nnz, const int64_t*
   c->normalized = (n > 0) && !bad;
   if (getenv("SKG_STORED_WEIGHTS")) c->normalized = false;  // experiment: read w, never recompute
   cudaFree(d_bad);
-  {  // graph-static range starts of the fused range expand (sampler.cu k_lad_range)
-    const int64_t nfr = (n + kFRange - 1) / kFRange;
-    if (c->normalized && nfr >= 1 && nfr <= kMaxFR) {
-      CK(cudaMalloc(&c->d_rstart, sizeof(int32_t) * (size_t)n * (nfr + 1)));
-      c->n_fr = (int32_t)nfr;
-      int rc = launch_build_rstart(c->gdev(), c->d_rstart, c->n_fr);
-      if (rc) return rc;
-      CK(cudaDeviceSynchronize());
-    }
-  }
+  // the fused range expand (sampler.cu k_lad_range) serves normalised graphs; its
+  // graph-static range-start table is built per range size when a plan set first needs it
+  c->fr_ok = c->normalized && n >= 1;
   if (!c->symmetric) {  // host counting sort by column (rows ascending within a column)
     std::vector<int64_t> toff(n + 1, 0);
     for (int64_t e = 0; e < nnz; ++e) toff[neighbors[e] + 1]++;
@@ -655,7 +656,7 @@ extern "C" int skg_ctx_destroy(skg_ctx* c) {
   cudaFree(c->d_trow);
   cudaFree(c->d_tw);
   cudaFree(c->d_degd);
-  cudaFree(c->d_rstart);
+  for (auto& kv : c->rstarts) cudaFree(kv.second);
   cudaFree(c->d_x);
   cudaFree(c->d_labels);
   cudaFree(c->d_ymulti);
@@ -850,6 +851,9 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     cap_cand = std::max<int64_t>(n, 1);
     cap_batch = 1;
   }
+  // per-layer arrays are strided by cap_cand: a multiple of 16 keeps every layer's norm and
+  // flag rows aligned for the vector loads of the pairwise leaves (k_pw_leaves)
+  cap_cand = (cap_cand + 15) / 16 * 16;
   ARG(cap_pairs < (1LL << 31) && cap_cand < (1LL << 31), "plan capacity exceeds int32 indexing");
   // LADIES keeps upper-row ranks in 16-bit slots / counters
   ARG(kind != KIND_LADIES || cap_rows < 65535, "LADIES batch / budget must be below 65535");
@@ -862,7 +866,34 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
   {
     const char* ex = getenv("SKG_EXPAND");
     const bool off = getenv("SKG_GLOBAL_EXPAND") || (ex && std::string(ex) != "fused");
-    ps->n_fr = (kind == KIND_LADIES && c->n_fr > 0 && !off && cap_rows <= kFusedMaxRows) ? c->n_fr : 0;
+    ps->n_fr = 0;
+    if (kind == KIND_LADIES && c->fr_ok && !off && cap_rows <= kFusedMaxRows) {
+      const int max_upper = L > 1 ? (int)std::max<int64_t>(cap_batch, std::min<int64_t>(budget, cap_cand))
+                                  : (int)cap_batch;
+      int nfr = 0;
+      const int fr = choose_fr(n, n_slots, max_upper, &nfr);
+      if (fr > 0 && nfr >= 1 && nfr <= kMaxFR) {
+        auto it = c->rstarts.find(fr);
+        if (it == c->rstarts.end()) {
+          int32_t* tab = nullptr;
+          CK(cudaMalloc(&tab, sizeof(int32_t) * (size_t)n * (nfr + 1)));
+          GraphDev g = c->gdev();
+          g.fr_size = fr;
+          int rc = launch_build_rstart(g, tab, nfr);
+          if (rc) {
+            cudaFree(tab);
+            return rc;
+          }
+          CK(cudaDeviceSynchronize());
+          it = c->rstarts.emplace(fr, tab).first;
+        }
+        ps->n_fr = nfr;
+        ps->fr_size = fr;
+        if (getenv("SKG_DEBUG_FR"))
+          fprintf(stderr, "skg: fused expand %d ranges x %d nodes for %d plans\n", nfr, fr, n_slots);
+        ps->rstart = it->second;
+      }
+    }
   }
   const int Ls = kind == KIND_LADIES ? L : 1;
   int pw = 0;

@@ -26,10 +26,10 @@ struct GraphDev {
   int32_t normalized;    // every w_ij == 1/sqrt(d_i d_j) (graph.py:182), checked at load
   const double* degd;    // [n] row lengths as double (normalized graphs)
   // fused range expand: rstart[i * (n_fr + 1) + q] = offset in row i of its first column
-  // >= q * kFRange (q = n_fr: the row length); graph-static, built at load
+  // >= q * fr_size (q = n_fr: the row length); graph-static per range size, built once
   const int32_t* rstart;
   int32_t n_fr;
-  int32_t pad_;
+  int32_t fr_size;
 };
 
 // Per-layer scalars of one plan.  Layers are indexed top-down while sampling
@@ -142,8 +142,7 @@ struct PlanDev {
 };
 
 constexpr int kSlots = 4;         // contributions kept per node before overflowing
-constexpr int kFRangeShift = 14;  // fused range expand: 16K nodes per range CTA
-constexpr int kFRange = 1 << kFRangeShift;
+constexpr int kFrGrain = 2048;   // fused range expand: range sizes are multiples of this
 constexpr int kMaxFR = 32;        // at most this many ranges (graphs up to 512K nodes)
 constexpr int kFusedMaxRows = 8192;  // upper rows per plan on the fused path
 constexpr int kRangeNodes = 65536;  // nodes per CTA of the shared-memory-counting expand
@@ -164,6 +163,9 @@ int launch_pull_norms(const GraphDev& g, const int32_t* cand, int32_t n_cand,
                       const uint32_t* row_bitmap, double* out, int32_t* err, cudaStream_t st);
 // GraphDev.rstart for a graph of n_fr ranges (stream 0, synchronous use at load)
 int launch_build_rstart(const GraphDev& g, int32_t* rstart, int n_fr);
+// fused range expand: range size (nodes per CTA, returned) and count for np plans per launch
+int choose_fr(int64_t n, int np, int max_upper, int* n_fr);
+size_t fr_smem_bytes(int fr_size, int ud_cap);
 void launch_set_bitmap(const int32_t* ids, int32_t n, uint32_t* bitmap, int32_t n_words,
                        cudaStream_t st);
 extern unsigned long long g_kernel_launches;
