@@ -199,3 +199,52 @@ def test_older_expand_paths_on_reddit_goldens(path):
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert "3 passed" in r.stdout, r.stdout[-2000:]
+
+
+# ------------------------------------------------------------ full-graph evaluation at shape
+@pytest.mark.parametrize("dtype,rtol", [("float64", 1e-9), ("float32", 1e-4)])
+def test_predict_logits_reddit_s_vs_oracle(dtype, rtol):
+    """predict_logits (training.py:325-334) on the 40K-node / 2M-edge reduced Reddit shape,
+    dims [602, 256 x 4, 41], against the CPU oracle's (P @ h) @ W chain in fp64."""
+    import paper_2101_07706_b200 as pkg
+    from golden_util import oracle_graph_from_shaped
+    sg = shaped("reddit_s")
+    og = oracle_graph_from_shaped(sg)
+    dims = [602, 256, 256, 256, 256, 41]
+    ws = O.init_model(dims, 0)
+    ref = O.predict_logits(ws, og)
+    pkg.set_compute_dtype(dtype)
+    try:
+        got = pkg.predict_logits(pkg.GcnModel([w.copy() for w in ws]), pkg.from_shaped(sg))
+    finally:
+        pkg.set_compute_dtype("float64")
+    scale = float(np.abs(ref).max())
+    np.testing.assert_allclose(got, ref, rtol=rtol, atol=rtol * scale)
+
+
+@pytest.mark.parametrize("dtype,rtol", [("float64", 1e-9), ("float32", 1e-4)])
+def test_predict_logits_full_reddit_vs_torch_sparse(dtype, rtol):
+    """predict_logits at the full Reddit shape (232,965 nodes, 113.5M CSR entries, 602-d):
+    compared with an independent fp64 chain on the device (torch CSR sparse @ dense, then
+    dense GEMM; the CPU oracle would need minutes for the 114M x 602 product)."""
+    import torch
+    import paper_2101_07706_b200 as pkg
+    sg = shaped("reddit", device="cuda")
+    dims = [602, 256, 256, 256, 256, 41]
+    ws = O.init_model(dims, 0)
+    Pm = torch.sparse_csr_tensor(torch.as_tensor(sg.offsets, device="cuda"),
+                                 torch.as_tensor(sg.neighbors.astype(np.int64), device="cuda"),
+                                 torch.as_tensor(sg.weights, device="cuda"),
+                                 size=(sg.n_nodes, sg.n_nodes))
+    h = torch.as_tensor(sg.features, device="cuda").double()
+    for l, w in enumerate(ws):
+        h = (Pm @ (h.clamp_min(0.0) if l else h)) @ torch.as_tensor(w, device="cuda")
+    ref = h.cpu().numpy()
+    del Pm, h
+    pkg.set_compute_dtype(dtype)
+    try:
+        got = pkg.predict_logits(pkg.GcnModel([w.copy() for w in ws]), pkg.from_shaped(sg))
+    finally:
+        pkg.set_compute_dtype("float64")
+    scale = float(np.abs(ref).max())
+    np.testing.assert_allclose(got, ref, rtol=rtol, atol=rtol * scale)
