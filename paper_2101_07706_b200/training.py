@@ -18,6 +18,7 @@ initialised, and the optimizer step is one fused kernel.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import warnings
 from dataclasses import dataclass, field, replace
 
@@ -628,7 +629,8 @@ class Trainer:
         self.stream = D.current_stream()
         self.main = torch.cuda.current_stream()
         # high priority: the sampler is the longer stage; GCN kernels fill its idle SMs
-        self.sides = [torch.cuda.Stream(priority=-1) for _ in range(self.n_streams)]
+        prio = int(os.environ.get("SKG_SAMPLER_PRIO", "-1"))
+        self.sides = [torch.cuda.Stream(priority=prio) for _ in range(self.n_streams)]
         self.side = self.sides[0]
         self.ev_sampled = [torch.cuda.Event() for _ in range(self.n_bufs)]
         self.ev_used = [torch.cuda.Event() for _ in range(self.n_bufs)]
