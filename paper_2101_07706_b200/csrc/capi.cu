@@ -377,11 +377,17 @@ struct skg_gcn {
   std::vector<char*> U, H;
   char* G0 = nullptr;
   char* G1 = nullptr;
+  char* G2 = nullptr;  // G alternates G0 / G2 layer by layer (dW reads one, SpMM^T writes the other)
+  // backward branch: dW_l and its slot reduction run on `side`, off the dX -> SpMM^T chain;
+  // ev[l] forks it, ev[L + l] marks dW_l done, ev[2L] joins (captured as graph edges)
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> ev;
   // TF32 lo parts of the tensor-core GEMM operands (fp32 only): U_l, G, and the weights'
   // padded hi / lo copies (row stride ldw[l] = round4(d_{l+1}))
   std::vector<char*> Ulo, Wh, Wl;
   std::vector<int64_t> ldw;
   char* G0lo = nullptr;
+  char* G2lo = nullptr;
   char* parts = nullptr;  // split-K partials of dW, one d_l x d_{l+1} block per slot
   int loss_kind = 0;      // 0: softmax cross-entropy (training.py:293-308); 1: multi-label BCE
   double pos_weight = 1.0;
@@ -1493,6 +1499,7 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   for (int l = 1; l <= L; ++l) cv.add(g->H[l], (size_t)S * R * g->ld[l] * es);
   cv.add(g->G0, (size_t)S * R * g->ld_max * es);
   cv.add(g->G1, (size_t)S * R * g->ld_max * es);
+  cv.add(g->G2, (size_t)S * R * g->ld_max * es);
   if (dtype == DT_F32) {
     g->Ulo.resize(L);
     g->Wh.resize(L);
@@ -1505,6 +1512,7 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
       cv.add(g->Wl[l], (size_t)dims[l] * g->ldw[l] * es);
     }
     cv.add(g->G0lo, (size_t)S * R * g->ld_max * es);
+    cv.add(g->G2lo, (size_t)S * R * g->ld_max * es);
   }
   cv.add(g->parts, (size_t)S * kMaxKSplit * wmax * es);
   cv.add(g->row_loss, (size_t)S * R);
@@ -1515,6 +1523,9 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   CK(cudaMalloc(&g->arena, cv.off));
   CK(cudaMemset(g->arena, 0, cv.off));
   cv.bind(g->arena);
+  CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+  g->ev.resize(2 * L + 1);
+  for (auto& e : g->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // descriptors: pointers into the plan arena are fixed for the plan set's lifetime
   std::vector<LayerDesc> hl((size_t)L * S);
   std::vector<const int32_t*> hr((size_t)L * S);
@@ -1563,6 +1574,8 @@ extern "C" int skg_gcn_set_loss(skg_gcn* g, int kind, double pos_weight) {
 extern "C" int skg_gcn_destroy(skg_gcn* g) {
   if (!g) return SKG_OK;
   g->graphs.clear();
+  for (cudaEvent_t e : g->ev) cudaEventDestroy(e);
+  if (g->side) cudaStreamDestroy(g->side);
   if (g->graphs.cap) cudaStreamDestroy(g->graphs.cap);
   if (g->loss_scratch) cudaFree(g->loss_scratch);
   cudaFree(g->arena);
@@ -1673,9 +1686,14 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
   }
   g_gemm_layer = -1;
   if (!backward) return SKG_OK;
-  Act<T> G = act<T>(g->G0, R, g->ld_max, g->ld[L], z0);
+  // G alternates between G0 and G2: the dW GEMM of layer l (on the side stream) reads the
+  // buffer the transposed SpMM of layer l - 1 would otherwise overwrite
+  char* Gb[2] = {g->G0, g->G2};
+  char* Gl[2] = {g->G0lo, g->G2lo};
+  int cur = 0;
+  Act<T> G = act<T>(Gb[0], R, g->ld_max, g->ld[L], z0);
   Act<T> Gu = act<T>(g->G1, R, g->ld_max, g->ld[L], z0);
-  T* G_lo = F32 ? lo_of(g->G0lo, g->ld_max) : nullptr;
+  T* G_lo = F32 ? lo_of(Gl[0], g->ld_max) : nullptr;
   if (g->loss_kind == 1) {
     if (!c->d_ymulti || c->y_classes != g->dims[L]) {
       set_error("multi-label BCE needs multi-hot labels with one bit per output class");
@@ -1687,11 +1705,15 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     softmax_ce_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
                     (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, loss, g->nlab + z0, st);
   }
+  cudaStream_t sd = g->side;
   for (int l = L - 1; l >= 0; --l) {
     const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
     const int32_t* const* rows = g->d_rows + (size_t)l * S + z0;
     const int dl = (int)g->dims[l], dn = (int)g->dims[l + 1];
-    // dW_l = sum_slots U_l^T G (split-K over slots, reduced in slot order)
+    // dW_l = sum_slots U_l^T G (split-K over slots, reduced in slot order), on the side
+    // stream: nothing on the dX -> SpMM^T chain waits for it
+    CK(cudaEventRecord(g->ev[l], st));
+    CK(cudaStreamWaitEvent(sd, g->ev[l], 0));
     Act<T> P;
     P.base = reinterpret_cast<T*>(g->parts);
     P.stride = g->part_elems;
@@ -1703,34 +1725,40 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
         g_gemm_layer = l;
         ks = gemm_tc_ksplit(n, dl, dn, Ri);
         rc = gemm_tc(mode, true, false, n, dl, dn, Ri, nullptr, rows, op(g->U[l], g->Ulo[l], g->ld[l], g->ld[l]),
-                     op(g->G0, g->G0lo, g->ld_max, G.ld), P, false, st, ks);
+                     op(Gb[cur], Gl[cur], g->ld_max, G.ld), P, false, sd, ks);
         if (rc) return rc;
         done = true;
       }
     }
     if (!done)
       gemm_simt<T>(true, false, n, dl, dn, Ri, nullptr, rows, act<T>(g->U[l], R, g->ld[l], g->ld[l], z0), G,
-                   P, false, st);
-    reduce_slots<T>(P.base, P.stride, n * ks, dl, dn, dn, reinterpret_cast<T*>(gp[l]), dn, accum, st);
+                   P, false, sd);
+    reduce_slots<T>(P.base, P.stride, n * ks, dl, dn, dn, reinterpret_cast<T*>(gp[l]), dn, accum, sd);
+    CK(cudaEventRecord(g->ev[L + l], sd));
     if (l == 0) break;
     // G_u = G W_l^T ; G <- (Block_l^T G_u) * [H_l > 0]
     Gu.ld = g->ld[l];
     done = false;
     if constexpr (F32) {
       if (tc) {
-        rc = gemm_tc(mode, false, true, n, Ri, dl, dn, rows, nullptr, op(g->G0, g->G0lo, g->ld_max, G.ld), wop(l),
+        g_gemm_layer = l;
+        rc = gemm_tc(mode, false, true, n, Ri, dl, dn, rows, nullptr, op(Gb[cur], Gl[cur], g->ld_max, G.ld), wop(l),
                      Gu, false, st);
         if (rc) return rc;
         done = true;
       }
     }
     if (!done) gemm_simt<T>(false, true, n, Ri, dl, dn, rows, nullptr, G, W(l), Gu, false, st);
-    Act<T> Gn = G;
-    Gn.ld = g->ld[l];
-    spmm_b<T>(lds, n, Ri, true, false, Gu, act<T>(g->H[l], R, g->ld[l], g->ld[l], z0), Gn, G_lo,
-              g->ld[l], st);
+    // the other G buffer was read by dW_{l+1}
+    if (l + 1 < L) CK(cudaStreamWaitEvent(st, g->ev[L + l + 1], 0));
+    Act<T> Gn = act<T>(Gb[cur ^ 1], R, g->ld_max, g->ld[l], z0);
+    spmm_b<T>(lds, n, Ri, true, false, Gu, act<T>(g->H[l], R, g->ld[l], g->ld[l], z0), Gn,
+              F32 ? lo_of(Gl[cur ^ 1], g->ld_max) : nullptr, g->ld[l], st);
     G = Gn;
+    cur ^= 1;
   }
+  CK(cudaEventRecord(g->ev[2 * L], sd));  // join: the step ends when every dW is reduced
+  CK(cudaStreamWaitEvent(st, g->ev[2 * L], 0));
   g_gemm_layer = -1;
   return SKG_OK;
 }
