@@ -379,7 +379,8 @@ struct skg_gcn {
   char* G1 = nullptr;
   char* G2 = nullptr;  // G alternates G0 / G2 layer by layer (dW reads one, SpMM^T writes the other)
   // backward branch: dW_l and its slot reduction run on `side`, off the dX -> SpMM^T chain;
-  // ev[l] forks it, ev[L + l] marks dW_l done, ev[2L] joins (captured as graph edges)
+  // ev[l] forks it, ev[L + l] marks dW_l done, ev[2L] joins (captured as graph edges);
+  // ev[2L + 1..3]: the weight split / label count branch at the start, the loss mean
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> ev;
   // TF32 lo parts of the tensor-core GEMM operands (fp32 only): U_l, G, and the weights'
@@ -1524,7 +1525,7 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   CK(cudaMemset(g->arena, 0, cv.off));
   cv.bind(g->arena);
   CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
-  g->ev.resize(2 * L + 1);
+  g->ev.resize(2 * L + 4);
   for (auto& e : g->ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // descriptors: pointers into the plan arena are fixed for the plan set's lifetime
   std::vector<LayerDesc> hl((size_t)L * S);
@@ -1650,6 +1651,13 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     o.rows_cap = g->dims[l];
     return o;
   };
+  // side branch at the start: the TF32 weight split (needed by the first GEMM) and the
+  // labelled-row count (needed by the softmax) run beside the gather and the first SpMM
+  cudaStream_t sd = g->side;
+  const bool soft = backward && g->loss_kind == 0;
+  CK(cudaEventRecord(g->ev[2 * L + 1], st));
+  CK(cudaStreamWaitEvent(sd, g->ev[2 * L + 1], 0));
+  if (soft) count_labels_b(g->d_slots + z0, n, c->d_labels, g->nlab + z0, sd);
   if (tc) {
     WSplitTable t;
     t.L = L;
@@ -1661,8 +1669,9 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
       t.cols[l] = g->dims[l + 1];
       t.ld_out[l] = g->ldw[l];
     }
-    split_weights(t, st);
+    split_weights(t, sd);
   }
+  CK(cudaEventRecord(g->ev[2 * L + 2], sd));
   Act<T> X0 = act<T>(g->X0, R, g->ld[0], g->ld[0], z0);
   gather_rows_b<T>(c->fstore(), g->d_slots + z0, n, Ri, X0, st);
   for (int l = 0; l < L; ++l) {
@@ -1671,6 +1680,7 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     Act<T> A = l == 0 ? X0 : act<T>(g->H[l], R, g->ld[l], g->ld[l], z0);
     Act<T> U = act<T>(g->U[l], R, g->ld[l], g->ld[l], z0);
     spmm_b<T>(lds, n, Ri, false, l > 0, A, A, U, F32 ? lo_of(g->Ulo[l], g->ld[l]) : nullptr, g->ld[l], st);
+    if (l == 0) CK(cudaStreamWaitEvent(st, g->ev[2 * L + 2], 0));  // split weights, label counts
     Act<T> Hn = act<T>(g->H[l + 1], R, g->ld[l + 1], g->ld[l + 1], z0);
     if constexpr (F32) {
       if (tc) {
@@ -1702,10 +1712,13 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     bce_b<T>(g->d_slots + z0, n, Ri, c->d_ymulti, c->y_words, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
              (int)g->dims[L], g->pos_weight, G, G_lo, g->row_loss + (size_t)z0 * R, loss, st);
   } else {
-    softmax_ce_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
-                    (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, loss, g->nlab + z0, st);
+    softmax_ce_rows_b<T>(g->d_slots + z0, n, Ri, c->d_labels, act<T>(g->H[L], R, g->ld[L], g->ld[L], z0),
+                         (int)g->dims[L], G, G_lo, g->row_loss + (size_t)z0 * R, g->nlab + z0, st);
+    // the fixed-order loss mean runs beside the backward chain
+    CK(cudaEventRecord(g->ev[2 * L + 3], st));
+    CK(cudaStreamWaitEvent(sd, g->ev[2 * L + 3], 0));
+    loss_mean_b(g->d_slots + z0, n, Ri, c->d_labels, g->row_loss + (size_t)z0 * R, g->nlab + z0, loss, sd);
   }
-  cudaStream_t sd = g->side;
   for (int l = L - 1; l >= 0; --l) {
     const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
     const int32_t* const* rows = g->d_rows + (size_t)l * S + z0;

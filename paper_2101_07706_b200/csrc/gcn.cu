@@ -446,13 +446,28 @@ __global__ void __launch_bounds__(1024) k_loss_mean(const SlotDesc* sd, const in
   }
 }
 
+void count_labels_b(const SlotDesc* sd, int n, const int32_t* labels, int32_t* nlab, cudaStream_t st) {
+  launch_k("k_count_labels", st, dim3(n), dim3(1024), 0, k_count_labels, sd, labels, nlab);
+}
+
+void loss_mean_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, const double* row_loss,
+                 const int32_t* nlab, double* loss_out, cudaStream_t st) {
+  launch_k("k_loss_mean", st, dim3(n), dim3(1024), 0, k_loss_mean, sd, labels, row_loss, (int64_t)max_rows,
+           nlab, loss_out);
+}
+
+template <typename T>
+void softmax_ce_rows_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
+                       Act<T> G, T* G_lo, double* row_loss, const int32_t* nlab, cudaStream_t st) {
+  launch_k("k_softmax_ce_b", st, dim3(dim3(row_blocks(max_rows, n), n)), dim3(256), 0, k_softmax_ce_b<T>, sd, labels, Z, C, G, G_lo, max_rows, row_loss, max_rows, nlab);
+}
+
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
                   Act<T> G, T* G_lo, double* row_loss, double* loss_out, int32_t* nlab, cudaStream_t st) {
-  launch_k("k_count_labels", st, dim3(n), dim3(1024), 0, k_count_labels, sd, labels, nlab);
-  launch_k("k_softmax_ce_b", st, dim3(dim3(row_blocks(max_rows, n), n)), dim3(256), 0, k_softmax_ce_b<T>, sd, labels, Z, C, G, G_lo, max_rows, row_loss, max_rows, (const int32_t*)nlab);
-  launch_k("k_loss_mean", st, dim3(n), dim3(1024), 0, k_loss_mean, sd, labels, row_loss, (int64_t)max_rows,
-           (const int32_t*)nlab, loss_out);
+  count_labels_b(sd, n, labels, nlab, st);
+  softmax_ce_rows_b<T>(sd, n, max_rows, labels, Z, C, G, G_lo, row_loss, nlab, st);
+  loss_mean_b(sd, n, max_rows, labels, row_loss, nlab, loss_out, st);
 }
 
 // ------------------------------------------------------------------ multi-label BCE
@@ -603,6 +618,8 @@ void fill_zero(T* p, int64_t n, cudaStream_t st) {
                                 bool, cudaStream_t);                                                \
   template void softmax_ce_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>, T*, \
                                 double*, double*, int32_t*, cudaStream_t);                          \
+  template void softmax_ce_rows_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>, \
+                                     T*, double*, const int32_t*, cudaStream_t);                    \
   template void bce_b<T>(const SlotDesc*, int, int, const uint64_t*, int, Act<T>, int, double, Act<T>, \
                          T*, double*, double*, cudaStream_t);                                       \
   template void sgd_step<T>(T*, const T*, int64_t, double, double, cudaStream_t);                   \

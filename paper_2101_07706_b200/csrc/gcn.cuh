@@ -112,6 +112,14 @@ void reduce_slots(const T* parts, int64_t part_stride, int n, int64_t rows, int6
 template <typename T>
 void softmax_ce_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
                   Act<T> G, T* G_lo, double* row_loss, double* loss_out, int32_t* nlab, cudaStream_t st);
+// its three parts (labelled-row count per slot, per-row gradient + loss, fixed-order mean),
+// for callers that run the count and the mean on a side branch
+void count_labels_b(const SlotDesc* sd, int n, const int32_t* labels, int32_t* nlab, cudaStream_t st);
+void loss_mean_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, const double* row_loss,
+                 const int32_t* nlab, double* loss_out, cudaStream_t st);
+template <typename T>
+void softmax_ce_rows_b(const SlotDesc* sd, int n, int max_rows, const int32_t* labels, Act<T> Z, int C,
+                       Act<T> G, T* G_lo, double* row_loss, const int32_t* nlab, cudaStream_t st);
 // multi-label BCE-with-logits (pos_weight on positives), mean over rows x C; multi-hot
 // targets y (y_words 64-bit words per node); G (+ TF32 G_lo, tail rows zeroed)
 template <typename T>
