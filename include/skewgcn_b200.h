@@ -102,6 +102,13 @@ int skg_ctx_destroy(skg_ctx* ctx);
  * dtype SKG_DT_F32 / SKG_DT_F64.  Stored padded to a multiple of 4 elements. */
 int skg_ctx_set_features(skg_ctx* ctx, int dtype, int64_t dim, int64_t n_rows,
                          const void* host_rows);
+/* Multi-hot (0/1) features bit-packed (the YouTube shape's 2048-d
+ * multi-hot rows; the reference keeps a dense float matrix, graph.py:30 Graph.features):
+ * n_rows x words_per_row uint32, feature c at bit (c & 31) of word (c >> 5).  The layer-0
+ * SpMM expands the bits to exact 0 / 1 in the compute dtype (dtype), so results equal
+ * skg_ctx_set_features on the unpacked rows.  Shards uploaded afterwards are packed rows. */
+int skg_ctx_set_features_bits(skg_ctx* ctx, int dtype, int64_t dim, int64_t n_rows,
+                              const uint32_t* host_words, int64_t words_per_row);
 /* Multi-GPU: feature rows are owned by ranks; node_rank/node_row give each node's home
  * (rank, row) and shard_ptrs the device pointers (local or NVLink-mapped peer) of every
  * rank's shard.  With one rank this is implicit (rank 0, row = node). */
@@ -118,7 +125,8 @@ int skg_ctx_set_multilabels(skg_ctx* ctx, const uint64_t* words, int32_t n_class
 int skg_ctx_set_labels(skg_ctx* ctx, const int64_t* labels);
 /* Replace the ownership map (Partition.owner) without re-uploading the CSR. */
 int skg_ctx_set_owner(skg_ctx* ctx, int32_t n_workers, const int32_t* owner);
-/* info: n, nnz, symmetric, feature_ld, feature_dim, feature_dtype, device */
+/* info: n, nnz, symmetric, feature_ld, feature_dim, feature_dtype, device,
+ * n_ranks | normalized << 32 | bit-packed features << 33 */
 int skg_ctx_info(skg_ctx* ctx, int64_t out[8]);
 
 /* CUDA IPC for peer feature shards over NVLink (one process per GPU). */

@@ -8,6 +8,7 @@ Importing this package requires the built library; there is no CPU fallback.
 
 from ._native import kernel_launches, lib as _lib  # noqa: F401  (fails loudly if missing)
 from ._device import compute_dtype, set_compute_dtype
+from .features import BitFeatures
 from .graph import (WeightedGraph, adjacency_block, column_norms, from_shaped, graph_from_edges,
                     load_edge_list, neighbor_union, node_set, normalize_weights, undirected_edges)
 from .partition import Partition, partition_nodes
@@ -23,7 +24,7 @@ from .training import (CommLedger, EvalResult, GcnModel, Metrics, MetricRow, Pla
 __version__ = "0.1.0"
 
 __all__ = [
-    "WeightedGraph", "adjacency_block", "column_norms", "neighbor_union", "node_set",
+    "BitFeatures", "WeightedGraph", "adjacency_block", "column_norms", "neighbor_union", "node_set",
     "normalize_weights", "graph_from_edges", "load_edge_list", "undirected_edges", "from_shaped",
     "Partition", "partition_nodes", "ProbDist", "SampleDraw", "SamplerConfig", "spawn_rng",
     "pcg64_state", "CommLedger", "EvalResult", "GcnModel", "Metrics", "MetricRow", "PlanLayer",

@@ -15,6 +15,7 @@ import weakref
 import numpy as np
 
 from ._native import DT, KIND_LADIES, KIND_SAINT, check, lib, ptr, require_device
+from .features import BitFeatures, auto_pack
 
 _COMPUTE = {"dtype": "float64"}
 
@@ -111,6 +112,7 @@ class DeviceGraph:
         self.owner_ref = None
         self.feat_key = None
         self.feat_ref = None
+        self.xbits = False
         self.lab_key = None
         self.lab_ref = None
         self.pool: dict = {}
@@ -141,15 +143,27 @@ class DeviceGraph:
             for ps in sets:
                 ps.train_key = None
 
-    def ensure_features(self, X: np.ndarray, dtype: str) -> None:
-        key = (id(X), X.__array_interface__["data"][0], X.shape, str(X.dtype), dtype)
+    def ensure_features(self, X, dtype: str) -> None:
+        """Upload the feature matrix: dense rows, or bit-packed rows for 0/1 (multi-hot)
+        features (a BitFeatures matrix, or a dense 0/1 one at least 256 wide)."""
+        if isinstance(X, BitFeatures):
+            key = ("bits", id(X), X.words.ctypes.data, X.shape, dtype)
+        else:
+            key = (id(X), X.__array_interface__["data"][0], X.shape, str(X.dtype), dtype)
         if key == self.feat_key:
             return
         if X.shape[0] != self.n:
             raise ValueError(f"feature rows ({X.shape[0]}) != n_nodes ({self.n})")
-        host = np.ascontiguousarray(X, dtype=np.float32 if dtype == "float32" else np.float64)
-        check(lib.skg_ctx_set_features(self.ctx, DT[dtype], host.shape[1], host.shape[0],
-                                       host.ctypes.data_as(C.c_void_p)))
+        if auto_pack(X):
+            bf = X if isinstance(X, BitFeatures) else BitFeatures.from_dense(X)
+            check(lib.skg_ctx_set_features_bits(self.ctx, DT[dtype], bf.dim, bf.shape[0],
+                                                bf.words.ctypes.data_as(C.c_void_p), bf.words.shape[1]))
+            self.xbits = True
+        else:
+            host = np.ascontiguousarray(X, dtype=np.float32 if dtype == "float32" else np.float64)
+            check(lib.skg_ctx_set_features(self.ctx, DT[dtype], host.shape[1], host.shape[0],
+                                           host.ctypes.data_as(C.c_void_p)))
+            self.xbits = False
         self.feat_key, self.feat_ref = key, X
         for sets in self.pool.values():
             for ps in sets:
@@ -171,7 +185,11 @@ class DeviceGraph:
 
     def upload_shard(self, rows: np.ndarray, dtype: str) -> int:
         """Copy host feature rows into their own device allocation (IPC-exportable)."""
-        host = np.ascontiguousarray(rows, dtype=np.float32 if dtype == "float32" else np.float64)
+        if self.xbits:  # the store holds packed rows: upload the shard packed too
+            bf = rows if isinstance(rows, BitFeatures) else BitFeatures.from_dense(rows)
+            host = bf.words
+        else:
+            host = np.ascontiguousarray(rows, dtype=np.float32 if dtype == "float32" else np.float64)
         out = C.c_uint64()
         check(lib.skg_ctx_shard_upload(self.ctx, host.ctypes.data_as(C.c_void_p), host.shape[0],
                                        C.byref(out)))

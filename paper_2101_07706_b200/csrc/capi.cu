@@ -177,6 +177,7 @@ struct skg_ctx {
   std::vector<int64_t> deg_desc_prefix;  // prefix sums of degrees sorted descending
   void* d_x = nullptr;
   int64_t F = 0, ldx = 0, x_rows = 0;
+  int xbits = 0;  // 1: d_x holds bit-packed multi-hot rows (ldx 32-bit words per row)
   int dtype = DT_F32;
   int32_t* d_labels = nullptr;
   // multi-label targets (multi-hot, y_words 64-bit words per node) for the BCE loss
@@ -214,6 +215,8 @@ struct skg_ctx {
     fs.node_row = d_node_row;
     fs.ld = ldx;
     fs.dim = F;
+    fs.bits = xbits;
+    fs.pad_ = 0;
     return fs;
   }
   int64_t edge_bound(int64_t rows) const {  // max sum of `rows` distinct row degrees
@@ -373,7 +376,6 @@ struct skg_gcn {
   int n_slots = 0;
   char* arena = nullptr;
   // layer-major activations: slot z of buffer X at X + z * R * ld(X) elements
-  char* X0 = nullptr;
   std::vector<char*> U, H;
   char* G0 = nullptr;
   char* G1 = nullptr;
@@ -687,11 +689,46 @@ extern "C" int skg_ctx_set_features(skg_ctx* c, int dtype, int64_t dim, int64_t 
   c->ldx = round4(dim);
   c->dtype = dtype;
   c->x_rows = n_rows;
+  c->xbits = 0;
   CK(cudaMalloc(&c->d_x, es * c->ldx * std::max<int64_t>(n_rows, 1)));
   CK(cudaMemset(c->d_x, 0, es * c->ldx * std::max<int64_t>(n_rows, 1)));
   if (n_rows)
     CK(cudaMemcpy2D(c->d_x, es * c->ldx, host_rows, es * dim, es * dim, n_rows, cudaMemcpyHostToDevice));
   // single-rank default map: shard 0 = all rows, row = node
+  cudaFree(c->d_shards);
+  CK(cudaMalloc(&c->d_shards, sizeof(uint64_t)));
+  uint64_t p = (uint64_t)c->d_x;
+  CK(cudaMemcpy(c->d_shards, &p, sizeof(uint64_t), cudaMemcpyHostToDevice));
+  c->n_ranks = 1;
+  cudaFree(c->d_node_rank);
+  cudaFree(c->d_node_row);
+  c->d_node_rank = nullptr;
+  c->d_node_row = nullptr;
+  return SKG_OK;
+}
+
+// Multi-hot (0 / 1) features bit-packed on the device: row i is words_per_row 32-bit words,
+// feature c at bit (c & 31) of word (c >> 5); expanded to 0 / 1 in the compute dtype by the
+// layer-0 SpMM (the same products as dense 0 / 1 rows, 32x fewer feature bytes).
+extern "C" int skg_ctx_set_features_bits(skg_ctx* c, int dtype, int64_t dim, int64_t n_rows,
+                                         const uint32_t* host_words, int64_t words_per_row) {
+  if (c) ++c->gen;
+  ARG(c && (dtype == DT_F32 || dtype == DT_F64) && dim > 0 && n_rows >= 0 &&
+          words_per_row >= (dim + 31) / 32 && (host_words || !n_rows),
+      "bad bit-packed feature arguments");
+  CK(cudaSetDevice(c->device));
+  cudaFree(c->d_x);
+  c->d_x = nullptr;
+  c->F = dim;
+  c->ldx = (((dim + 31) / 32) + 3) / 4 * 4;  // words, padded to 16 bytes
+  c->dtype = dtype;
+  c->x_rows = n_rows;
+  c->xbits = 1;
+  CK(cudaMalloc(&c->d_x, 4 * c->ldx * std::max<int64_t>(n_rows, 1)));
+  CK(cudaMemset(c->d_x, 0, 4 * c->ldx * std::max<int64_t>(n_rows, 1)));
+  if (n_rows)
+    CK(cudaMemcpy2D(c->d_x, 4 * c->ldx, host_words, 4 * words_per_row, 4 * ((dim + 31) / 32), n_rows,
+                    cudaMemcpyHostToDevice));
   cudaFree(c->d_shards);
   CK(cudaMalloc(&c->d_shards, sizeof(uint64_t)));
   uint64_t p = (uint64_t)c->d_x;
@@ -726,12 +763,14 @@ extern "C" int skg_ctx_shard_upload(skg_ctx* c, const void* host_rows, int64_t n
                                     uint64_t* out_dev_ptr) {
   ARG(c && c->d_x && n_rows >= 0 && out_dev_ptr, "set features before uploading shards");
   CK(cudaSetDevice(c->device));
-  const size_t es = c->dtype == DT_F32 ? 4 : 8;
+  // bit-packed features: host rows are ceil(F / 32) words each
+  const size_t es = c->xbits ? 4 : c->dtype == DT_F32 ? 4 : 8;
+  const int64_t in_elems = c->xbits ? (c->F + 31) / 32 : c->F;
   void* p = nullptr;
   CK(cudaMalloc(&p, es * c->ldx * std::max<int64_t>(n_rows, 1)));
   CK(cudaMemset(p, 0, es * c->ldx * std::max<int64_t>(n_rows, 1)));
   if (n_rows)
-    CK(cudaMemcpy2D(p, es * c->ldx, host_rows, es * c->F, es * c->F, n_rows, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy2D(p, es * c->ldx, host_rows, es * in_elems, es * in_elems, n_rows, cudaMemcpyHostToDevice));
   c->shards_owned.push_back(p);
   *out_dev_ptr = (uint64_t)p;
   return SKG_OK;
@@ -793,7 +832,7 @@ extern "C" int skg_ctx_info(skg_ctx* c, int64_t out[8]) {
   out[4] = c->F;
   out[5] = c->dtype;
   out[6] = c->device;
-  out[7] = c->n_ranks | ((int64_t)c->normalized << 32);
+  out[7] = c->n_ranks | ((int64_t)c->normalized << 32) | ((int64_t)c->xbits << 33);
   return SKG_OK;
 }
 
@@ -1495,7 +1534,6 @@ extern "C" int skg_gcn_create(skg_plans* ps, int L, const int64_t* dims, int dty
   g->U.resize(L);
   g->H.resize(L + 1);
   Carver cv;
-  cv.add(g->X0, (size_t)S * R * g->ld[0] * es);
   for (int l = 0; l < L; ++l) cv.add(g->U[l], (size_t)S * R * g->ld[l] * es);
   for (int l = 1; l <= L; ++l) cv.add(g->H[l], (size_t)S * R * g->ld[l] * es);
   cv.add(g->G0, (size_t)S * R * g->ld_max * es);
@@ -1672,14 +1710,17 @@ int gcn_run(skg_gcn* g, int z0, int n, const uint64_t* wp, const uint64_t* gp, b
     split_weights(t, sd);
   }
   CK(cudaEventRecord(g->ev[2 * L + 2], sd));
-  Act<T> X0 = act<T>(g->X0, R, g->ld[0], g->ld[0], z0);
-  gather_rows_b<T>(c->fstore(), g->d_slots + z0, n, Ri, X0, st);
   for (int l = 0; l < L; ++l) {
     const LayerDesc* lds = g->d_layers + (size_t)l * S + z0;
     const int32_t* const* rows = g->d_rows + (size_t)l * S + z0;
-    Act<T> A = l == 0 ? X0 : act<T>(g->H[l], R, g->ld[l], g->ld[l], z0);
     Act<T> U = act<T>(g->U[l], R, g->ld[l], g->ld[l], z0);
-    spmm_b<T>(lds, n, Ri, false, l > 0, A, A, U, F32 ? lo_of(g->Ulo[l], g->ld[l]) : nullptr, g->ld[l], st);
+    if (l == 0) {  // the X[S_0] gather (local or NVLink peer rows) fused into the first SpMM
+      spmm_in_b<T>(c->fstore(), g->d_slots + z0, lds, n, Ri, U, F32 ? lo_of(g->Ulo[0], g->ld[0]) : nullptr,
+                   g->ld[0], st);
+    } else {
+      Act<T> A = act<T>(g->H[l], R, g->ld[l], g->ld[l], z0);
+      spmm_b<T>(lds, n, Ri, false, true, A, A, U, F32 ? lo_of(g->Ulo[l], g->ld[l]) : nullptr, g->ld[l], st);
+    }
     if (l == 0) CK(cudaStreamWaitEvent(st, g->ev[2 * L + 2], 0));  // split weights, label counts
     Act<T> Hn = act<T>(g->H[l + 1], R, g->ld[l + 1], g->ld[l + 1], z0);
     if constexpr (F32) {
@@ -1896,7 +1937,11 @@ extern "C" int skg_predict_logits(skg_ctx* c, int L, const int64_t* dims, const 
     const int64_t ldo = last ? dims[L] : round4(dims[l + 1]);
     if (dtype == DT_F32) {
       const float* A = l == 0 ? (const float*)c->d_x : (const float*)H;
-      spmm_full<float>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (float*)U, ldl, ldl, st);
+      if (l == 0 && c->xbits)
+        spmm_full_bits<float>(c->n, c->d_off, c->d_col, c->d_w, (const uint32_t*)c->d_x, c->ldx, (float*)U, ldl,
+                              ldl, st);
+      else
+        spmm_full<float>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (float*)U, ldl, ldl, st);
       if (mode) {
         // P·(X·W) rounding differs from the fp64 reference only at fp32 level (3xTF32)
         float* uh = (float*)U;
@@ -1916,7 +1961,11 @@ extern "C" int skg_predict_logits(skg_ctx* c, int L, const int64_t* dims, const 
       }
     } else {
       const double* A = l == 0 ? (const double*)c->d_x : (const double*)H;
-      spmm_full<double>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (double*)U, ldl, ldl, st);
+      if (l == 0 && c->xbits)
+        spmm_full_bits<double>(c->n, c->d_off, c->d_col, c->d_w, (const uint32_t*)c->d_x, c->ldx, (double*)U,
+                               ldl, ldl, st);
+      else
+        spmm_full<double>(c->n, c->d_off, c->d_col, c->d_w, A, ldi, l > 0, (double*)U, ldl, ldl, st);
       gemm_plain<double>((int)c->n, (int)dims[l + 1], (int)dims[l], (const double*)U, ldl,
                          (const double*)wp[l], dims[l + 1], last ? (double*)out_dev : (double*)H, ldo,
                          st);

@@ -29,6 +29,7 @@ struct Vec4<float> {
   __device__ static Vec4 load(const float* p) { Vec4 r; r.v = *reinterpret_cast<const float4*>(p); return r; }
   __device__ void store(float* p) const { *reinterpret_cast<float4*>(p) = v; }
   __device__ static Vec4 zero() { Vec4 r; r.v = make_float4(0.f, 0.f, 0.f, 0.f); return r; }
+  __device__ static Vec4 from4(float4 f) { Vec4 r; r.v = f; return r; }
   __device__ void fma(float a, const Vec4& x) {
     v.x = fmaf(a, x.v.x, v.x); v.y = fmaf(a, x.v.y, v.y);
     v.z = fmaf(a, x.v.z, v.z); v.w = fmaf(a, x.v.w, v.w);
@@ -47,6 +48,7 @@ struct Vec4<double> {
   }
   __device__ void store(double* p) const { reinterpret_cast<double2*>(p)[0] = a; reinterpret_cast<double2*>(p)[1] = b; }
   __device__ static Vec4 zero() { Vec4 r; r.a = make_double2(0, 0); r.b = make_double2(0, 0); return r; }
+  __device__ static Vec4 from4(float4 f) { Vec4 r; r.a = make_double2(f.x, f.y); r.b = make_double2(f.z, f.w); return r; }
   __device__ void fma(double s, const Vec4& x) {
     a.x = ::fma(s, x.a.x, a.x); a.y = ::fma(s, x.a.y, a.y); b.x = ::fma(s, x.b.x, b.x); b.y = ::fma(s, x.b.y, b.y);
   }
@@ -73,31 +75,6 @@ static int row_blocks(int max_rows, int n) {
   int b = (max_rows + 7) / 8;
   int cap = std::max(1, (4 * sms() + n - 1) / n);
   return std::max(1, std::min(b, std::max(cap, 1)));
-}
-
-// ------------------------------------------------------------------ gather (K7)
-// X0[slot][c] = X[S_0[c]] from the owner's shard (local or NVLink peer pointer).
-template <typename T>
-__global__ void k_gather_b(FeatStore fs, const SlotDesc* sd, Act<T> out) {
-  SKG_PDL_PROLOGUE();
-  const SlotDesc d = sd[blockIdx.y];
-  const int n = *d.n_in;
-  T* o = out.at(blockIdx.y);
-  const int lane = threadIdx.x & 31;
-  const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
-    const int node = d.in_nodes[r];
-    const int rank = fs.node_rank ? fs.node_rank[node] : 0;
-    const int64_t row = fs.node_row ? fs.node_row[node] : node;
-    const T* src = reinterpret_cast<const T*>(fs.shards[rank]) + row * fs.ld;
-    for (int64_t c = lane * 4; c < fs.ld; c += 128) Vec4<T>::load(src + c).store(o + r * out.ld + c);
-  }
-}
-
-template <typename T>
-void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows, Act<T> out,
-                   cudaStream_t st) {
-  launch_k("k_gather_b", st, dim3(dim3(row_blocks(max_rows, n), n)), dim3(256), 0, k_gather_b<T>, fs, sd, out);
 }
 
 // ------------------------------------------------------------------ SpMM (K8 / K10)
@@ -178,6 +155,110 @@ void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu
   if (transposed) launch_k("k_spmm_b<T,1,0>", st, dim3(grid), dim3(256), 0, k_spmm_b<T, true, false>, ld, A, H, out, out_lo, max_rows, width);
   else if (relu_in) launch_k("k_spmm_b<F,1>", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, true>, ld, A, H, out, out_lo, max_rows, width);
   else launch_k("k_spmm_b<F,0>", st, dim3(grid), dim3(256), 0, k_spmm_b<T, false, false>, ld, A, H, out, out_lo, max_rows, width);
+}
+
+// ------------------------------------------------------------------ fused gather + SpMM
+// four features c .. c + 3 (c a multiple of 4) of a bit-packed row as 0 / 1
+template <typename T>
+__device__ __forceinline__ Vec4<T> bits4(const uint32_t* row, int64_t c) {
+  const uint32_t nib = (row[c >> 5] >> (c & 31)) & 0xFu;
+  float4 f = make_float4((float)(nib & 1u), (float)((nib >> 1) & 1u), (float)((nib >> 2) & 1u),
+                         (float)(nib >> 3));
+  return Vec4<T>::from4(f);
+}
+
+// out[r] = sum_p val[p] X[S_0[ix[p]]] over the layer-0 block's rows, X rows addressed through
+// the feature store; same per-column accumulation order as k_spmm_b over a gathered X_0
+template <typename T, bool BITS>
+__global__ void k_spmm_in_b(FeatStore fs, const SlotDesc* sd, const LayerDesc* lds, Act<T> out,
+                            T* out_lo, int max_rows, int64_t width) {
+  SKG_PDL_PROLOGUE();
+  const LayerDesc d = lds[blockIdx.y];
+  const int32_t* __restrict__ in_nodes = sd[blockIdx.y].in_nodes;
+  const int rows = *d.rows;
+  const int32_t* __restrict__ ip = d.indptr;
+  const int32_t* __restrict__ ix = d.indices;
+  const double* __restrict__ vv = d.val;
+  T* o = out.at(blockIdx.y);
+  T* ol = out_lo ? out_lo + (int64_t)blockIdx.y * out.stride : nullptr;
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int rows_all = ol ? max_rows : rows;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows_all; r += nw) {
+    if (r >= rows) {
+      for (int64_t c = lane * 4; c < width; c += 128) {
+        Vec4<T>::zero().store(o + (int64_t)r * out.ld + c);
+        Vec4<T>::zero().store(ol + (int64_t)r * out.ld + c);
+      }
+      continue;
+    }
+    const int b = ip[r], e = ip[r + 1];
+    constexpr int NB = 2;
+    for (int64_t c0 = lane * 4; c0 < width; c0 += 128 * NB) {
+      Vec4<T> acc[NB];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) acc[q] = Vec4<T>::zero();
+#pragma unroll 2
+      for (int p = b; p < e; ++p) {
+        const T s = (T)vv[p];
+        const int node = in_nodes[ix[p]];
+        const int rank = fs.node_rank ? fs.node_rank[node] : 0;
+        const int64_t row = fs.node_row ? fs.node_row[node] : node;
+#pragma unroll
+        for (int q = 0; q < NB; ++q) {
+          if (c0 + 128 * q < width) {
+            Vec4<T> x;
+            if (BITS) x = bits4<T>(reinterpret_cast<const uint32_t*>(fs.shards[rank]) + row * fs.ld, c0 + 128 * q);
+            else x = Vec4<T>::load(reinterpret_cast<const T*>(fs.shards[rank]) + row * fs.ld + c0 + 128 * q);
+            acc[q].fma(s, x);
+          }
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NB; ++q) {
+        const int64_t c = c0 + 128 * q;
+        if (c >= width) continue;
+        if (ol) store_split(acc[q], o + (int64_t)r * out.ld + c, ol + (int64_t)r * out.ld + c);
+        else acc[q].store(o + (int64_t)r * out.ld + c);
+      }
+    }
+  }
+}
+
+template <typename T>
+void spmm_in_b(const FeatStore& fs, const SlotDesc* sd, const LayerDesc* ld, int n, int max_rows,
+               Act<T> out, T* out_lo, int64_t width, cudaStream_t st) {
+  dim3 grid(row_blocks(max_rows, n), n);
+  if (fs.bits)
+    launch_k("k_spmm_in_b<bits>", st, dim3(grid), dim3(256), 0, k_spmm_in_b<T, true>, fs, sd, ld, out, out_lo,
+             max_rows, width);
+  else
+    launch_k("k_spmm_in_b", st, dim3(grid), dim3(256), 0, k_spmm_in_b<T, false>, fs, sd, ld, out, out_lo,
+             max_rows, width);
+}
+
+template <typename T>
+__global__ void k_spmm_full_bits(int64_t n, const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+                                 const double* __restrict__ w, const uint32_t* __restrict__ X, int64_t ldw,
+                                 T* __restrict__ out, int64_t ldo, int64_t width) {
+  SKG_PDL_PROLOGUE();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    const int64_t b = off[r], e = off[r + 1];
+    for (int64_t c = lane * 4; c < width; c += 128) {
+      Vec4<T> acc = Vec4<T>::zero();
+      for (int64_t p = b; p < e; ++p) acc.fma((T)w[p], bits4<T>(X + (int64_t)col[p] * ldw, c));
+      acc.store(out + r * ldo + c);
+    }
+  }
+}
+
+template <typename T>
+void spmm_full_bits(int64_t n, const int64_t* off, const int32_t* col, const double* w, const uint32_t* X,
+                    int64_t ldw, T* out, int64_t ldo, int64_t width, cudaStream_t st) {
+  launch_k("k_spmm_full_bits", st, dim3(16 * sms()), dim3(256), 0, k_spmm_full_bits<T>, n, off, col, w, X, ldw,
+           out, ldo, width);
 }
 
 // full-graph SpMM for predict_logits (int64 offsets)
@@ -609,13 +690,16 @@ void fill_zero(T* p, int64_t n, cudaStream_t st) {
 }
 
 #define INST(T)                                                                                     \
-  template void gather_rows_b<T>(const FeatStore&, const SlotDesc*, int, int, Act<T>, cudaStream_t); \
   template void spmm_b<T>(const LayerDesc*, int, int, bool, bool, Act<T>, Act<T>, Act<T>, T*,       \
                           int64_t, cudaStream_t);                                                   \
   template void gemm_simt<T>(bool, bool, int, int, int, int, const int32_t* const*,                 \
                              const int32_t* const*, Act<T>, Act<T>, Act<T>, bool, cudaStream_t);    \
   template void reduce_slots<T>(const T*, int64_t, int, int64_t, int64_t, int64_t, T*, int64_t,     \
                                 bool, cudaStream_t);                                                \
+  template void spmm_in_b<T>(const FeatStore&, const SlotDesc*, const LayerDesc*, int, int, Act<T>, T*, \
+                             int64_t, cudaStream_t);                                                \
+  template void spmm_full_bits<T>(int64_t, const int64_t*, const int32_t*, const double*,           \
+                                  const uint32_t*, int64_t, T*, int64_t, int64_t, cudaStream_t);   \
   template void softmax_ce_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>, T*, \
                                 double*, double*, int32_t*, cudaStream_t);                          \
   template void softmax_ce_rows_b<T>(const SlotDesc*, int, int, const int32_t*, Act<T>, int, Act<T>, \

@@ -14,8 +14,10 @@ struct FeatStore {
   const void* const* shards;  // device array [n_ranks] of shard base pointers
   const int32_t* node_rank;   // [n] rank holding node's row (null: all local, row == node)
   const int32_t* node_row;    // [n] row inside that rank's shard
-  int64_t ld;                 // elements per row (padded to a multiple of 4)
+  int64_t ld;                 // elements per row (padded to a multiple of 4); bits: 32-bit words
   int64_t dim;                // true feature dimension
+  int32_t bits;               // 1: multi-hot rows bit-packed (feature c = bit c & 31 of word c >> 5)
+  int32_t pad_;
 };
 
 // Block of bottom-up layer l of one slot (device pointers into the plan arena).
@@ -89,12 +91,19 @@ void split_tf32(const float* in, int64_t ld_in, int64_t rows, int64_t cols, floa
                 int64_t ld_out, cudaStream_t st);
 void split_weights(const WSplitTable& t, cudaStream_t st);
 
-template <typename T>
-void gather_rows_b(const FeatStore& fs, const SlotDesc* sd, int n, int max_rows, Act<T> out,
-                   cudaStream_t st);
 // out = Block_l (relu?(A))  or, transposed, out = (Block_l^T A) * [H > 0].
 // With out_lo (fp32 only) the result is written TF32-split (hi into out, lo into out_lo)
 // for the tensor-core GEMMs, and rows [rows, max_rows) of every slot are zeroed.
+// layer-0 SpMM fused with the feature gather: out = Block_0 . X[S_0], rows of X read
+// through the feature store (local shard or NVLink-mapped peer shard; fp32 / fp64 rows or
+// bit-packed multi-hot rows expanded to 0 / 1 on the fly)
+template <typename T>
+void spmm_in_b(const FeatStore& fs, const SlotDesc* sd, const LayerDesc* ld, int n, int max_rows,
+               Act<T> out, T* out_lo, int64_t width, cudaStream_t st);
+// full-graph SpMM over bit-packed rows (predict_logits layer 0)
+template <typename T>
+void spmm_full_bits(int64_t n, const int64_t* off, const int32_t* col, const double* w,
+                    const uint32_t* X, int64_t ldw, T* out, int64_t ldo, int64_t width, cudaStream_t st);
 template <typename T>
 void spmm_b(const LayerDesc* ld, int n, int max_rows, bool transposed, bool relu_in, Act<T> A,
             Act<T> H, Act<T> out, T* out_lo, int64_t width, cudaStream_t st);

@@ -22,6 +22,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
+from .features import BitFeatures, pack_rows
+
 # Shapes quoted in BASELINE.json:configs / SURVEY.md §8(d).  m is the number of
 # undirected edge draws before dedup (self-pairs dropped).
 SHAPES = {
@@ -74,6 +76,8 @@ class ShapedGraph:
         return h.hexdigest()
 
     def features_hash(self) -> str:
+        if isinstance(self.features, BitFeatures):  # packed rows: hash the words
+            return hashlib.sha256(self.features.words.tobytes()).hexdigest()
         return hashlib.sha256(np.ascontiguousarray(self.features).tobytes()).hexdigest()
 
 
@@ -137,8 +141,11 @@ def _normalised_csr_torch(u, v, n, device):
 
 
 def make_shaped_graph(name: str, seed: int = 0, device: str | None = None,
-                      with_features: bool = True) -> ShapedGraph:
-    """Build the named shape deterministically.  device='cuda' speeds up the sort."""
+                      with_features: bool = True, packed: bool = False) -> ShapedGraph:
+    """Build the named shape deterministically.  device='cuda' speeds up the sort.
+    packed=True returns bag-of-words (multi-hot) features as BitFeatures, generated in row
+    chunks from the same random stream (identical values; the YouTube shape's 2048-d rows
+    never exist densely on the host)."""
     s = SHAPES[name]
     n, m, F, C = s["n"], s["m"], s["F"], s["C"]
     root = np.random.SeedSequence([seed, int.from_bytes(name.encode()[:8].ljust(8, b"\0"), "little")])
@@ -154,6 +161,19 @@ def make_shaped_graph(name: str, seed: int = 0, device: str | None = None,
         if s["feat"] == "gauss":
             x = r_feat.standard_normal(size=(n, F), dtype=np.float32)
             x[np.arange(n), blocks % F] += np.float32(1.0)
+        elif packed:  # the same draws as below, packed 32 features per word as they come
+            words = np.zeros((n, (F + 31) // 32), dtype="<u4")
+            ch = max(1, (1 << 24) // F)
+            for s0 in range(0, n, ch):
+                xb = r_feat.random((min(ch, n - s0), F), dtype=np.float32) < 0.0127
+                words[s0:s0 + len(xb)] = pack_rows(xb)
+            sig = (blocks * 10) % F
+            for j in range(10):
+                on = r_feat.random(n) < 0.3
+                cols = (sig[on] + j) % F
+                np.bitwise_or.at(words, (np.flatnonzero(on), cols >> 5),
+                                 (np.uint32(1) << (cols & 31).astype(np.uint32)).astype("<u4"))
+            x = BitFeatures(words, F)
         else:  # Bernoulli bag of words with a block signal
             x = (r_feat.random((n, F), dtype=np.float32) < 0.0127).astype(np.float32)
             sig = (blocks * 10) % F
