@@ -976,6 +976,8 @@ extern "C" int skg_plans_create(skg_ctx* c, int kind, int n_slots, int L, int64_
     P.cap_tiles = cap_tiles;
     cv.add(P.bitmap, n_words);
     cv.add(P.sbitmap, n_words);
+    cv.add(P.bitmap1, (size_t)(n_words + 31) / 32);
+    cv.add(P.dirty, 1);
     cv.add(P.cnt_pack, ps->n_fr ? 1 : (size_t)(n / 2 + 1));
     const bool lad = kind == KIND_LADIES, stw = lad && !c->normalized;
     cv.add(P.slots, lad && !ps->n_fr ? (size_t)std::max<int64_t>(n, 1) * kSlots : 4);

@@ -77,6 +77,8 @@ struct PlanDev {
   // ---- scratch
   uint32_t* bitmap;         // [n_words]
   uint32_t* sbitmap;        // [n_words] sampled set
+  uint32_t* bitmap1;        // [ceil(n_words / 32)] global expand: nonzero words of bitmap (zero at rest)
+  int32_t* dirty;           // [1] a call failed with state that is zero at rest left set (arena, persistent)
   uint32_t* cnt_pack;       // [n/2+1] 16-bit pair counters per node, zero at rest
   // LADIES contributions (upper-row rank r of every pair (r, j)), by node: the first
   // kSlots arrivals in slots[j], later ones in the overflow list; candidates with more
