@@ -35,6 +35,7 @@ sys.path.insert(0, str(ROOT))
 METRIC = "LADIES 5-layer GCN iters/sec at 1/2/4/8 B200; remote nodes fetched/iter"
 DIMS_HIDDEN = 256
 N_LAYERS = 5
+PLANS_PER_LAUNCH = 40  # default sampler look-ahead, in plans (all workers of T iterations)
 
 
 def parse():
@@ -62,7 +63,7 @@ def parse_args(argv):
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ahead", type=int, default=0,
-                    help="iterations of plans per sampler launch (0: ceil(24 / workers per rank))")
+                    help="iterations of plans per sampler launch (0: ceil(40 / workers per rank))")
     ap.add_argument("--streams", type=int, default=2, help="sampler streams (groups in flight)")
     a = ap.parse_args(argv)
     if a.sampler == "auto":
@@ -319,10 +320,11 @@ def run_ours(args):
     cfg = P.SamplerConfig(budget=args.subgraph if saint else args.budget, skew_constant=args.D,
                           mode=args.mode)
     P.set_compute_dtype(args.dtype)
-    # plans per sampler launch stay ~24 whatever the rank count (k = 8 workers per step,
-    # spread over the ranks): look-ahead T = ceil(24 / workers on this rank)
+    # plans per sampler launch stay ~40 whatever the rank count (k = 8 workers per step,
+    # spread over the ranks): look-ahead T = ceil(40 / workers on this rank).  Measured on
+    # one B200 (Reddit LADIES): T = 3 / 4 / 5 / 6 -> 2030 / 2077 / 2095 / 2051 it/s
     n_my_est = max(1, len(P.training.assign_workers(list(range(k)), rank, world)))
-    T = args.ahead if args.ahead > 0 else max(1, -(-24 // n_my_est))
+    T = args.ahead if args.ahead > 0 else max(1, -(-PLANS_PER_LAUNCH // n_my_est))
     tr = P.Trainer(g, part, model, cfg, batch_size=args.batch, lr=args.lr, mode=args.mode,
                    seed=0, dtype=args.dtype, epochs=1, ahead=T, streams=args.streams,
                    sampler=args.sampler, subgraph_size=args.subgraph if saint else None)

@@ -22,7 +22,17 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .features import BitFeatures, pack_rows
+try:
+    from .features import BitFeatures, pack_rows
+except ImportError:  # loaded by path (bench.py's reference arm never imports the package)
+    import importlib.util as _ilu
+    import sys as _sys
+    from pathlib import Path as _Path
+    _spec = _ilu.spec_from_file_location("skg_features", _Path(__file__).with_name("features.py"))
+    _feat = _ilu.module_from_spec(_spec)
+    _sys.modules.setdefault("skg_features", _feat)
+    _spec.loader.exec_module(_feat)
+    BitFeatures, pack_rows = _feat.BitFeatures, _feat.pack_rows
 
 # Shapes quoted in BASELINE.json:configs / SURVEY.md §8(d).  m is the number of
 # undirected edge draws before dedup (self-pairs dropped).
