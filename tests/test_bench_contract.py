@@ -57,7 +57,7 @@ def test_bench_spawns_ranks_gloo():
     out = json.loads(lines[0])
     assert out["n_gpus"] == 2 and out["steps"] == 6 and out["warmup"] == 3
     assert out["pipeline"]["workers_this_rank"] == 4
-    assert out["pipeline"]["plans_per_sampler_launch"] == 24  # ceil(24 / 4) iterations ahead
+    assert out["pipeline"]["plans_per_sampler_launch"] == 40  # ceil(40 / 4) iterations ahead
     assert out["exchange"]["remote_input_rows_per_iter"] > 0
     assert out["allreduce"]["bytes"] > 0 and out["allreduce"]["backend"] == "gloo"
     assert out["e2e"]["value"] > 0 and out["gpu_launches"] > 0
