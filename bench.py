@@ -410,6 +410,9 @@ def run_ours(args):
     barrier()
     launches0 = P.kernel_launches()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fr_trace = os.environ.get("SKG_FR_TRACE")  # diagnostic: range-expand CTA timeline
+    if fr_trace:
+        lib.skg_debug_fr_trace(1, None)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
@@ -431,6 +434,11 @@ def run_ours(args):
         barrier()
     launches = P.kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1)
+    if fr_trace:
+        buf = (C.c_ulonglong * (8 * 32 * 9))()
+        lib.skg_debug_fr_trace(0, buf)
+        with open(fr_trace, "w") as fh:
+            json.dump(list(buf), fh)
     if dist is not None:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
