@@ -320,6 +320,9 @@ def run_ours(args):
     cfg = P.SamplerConfig(budget=args.subgraph if saint else args.budget, skew_constant=args.D,
                           mode=args.mode)
     P.set_compute_dtype(args.dtype)
+    # the Trainer's GCN runs on the caller's stream: a high-priority one (the sampler streams
+    # run at the lowest priority), as train_distributed does
+    torch.cuda.set_stream(torch.cuda.Stream(priority=int(os.environ.get("SKG_MAIN_PRIO", "-1"))))
     # plans per sampler launch stay ~40 whatever the rank count (k = 8 workers per step,
     # spread over the ranks): look-ahead T = ceil(40 / workers on this rank).  Measured on
     # one B200 (Reddit LADIES): T = 3 / 4 / 5 / 6 -> 2030 / 2077 / 2095 / 2051 it/s

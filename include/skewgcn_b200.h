@@ -90,6 +90,14 @@ int skg_choice_noreplace(const uint64_t state[4], int has_uint32, uint32_t uinte
 int skg_iteration_inputs(uint64_t master_seed, int64_t epoch, int64_t it, int64_t worker,
                          const int64_t* train_w, int64_t n_train_w, int64_t batch_size,
                          int64_t* out_batch, int64_t* out_len, uint64_t plan_state[4]);
+/* skg_iteration_inputs for n worker-iterations (a look-ahead group of training.py:
+ * 488-493 iterations) on up to n_threads host threads: item i = (epochs[i], its[i],
+ * workers[i]) over train_ptrs[i] (int64 node ids, train_lens[i] of them); batch i packed
+ * at out_batch[out_off[i] .. out_off[i+1]), plan state at plan_states[4i..4i+3]. */
+int skg_group_inputs(uint64_t master_seed, int n, const int64_t* epochs, const int64_t* its,
+                     const int32_t* workers, const uint64_t* train_ptrs, const int64_t* train_lens,
+                     int64_t batch_size, int64_t* out_batch, int64_t* out_off,
+                     uint64_t* plan_states, int n_threads);
 
 /* ---------------------------------------------------------------- graph store
  * WeightedGraph (graph.py:20-79) + Partition.owner (partition.py:21) replicated on one

@@ -50,6 +50,8 @@ _sig("skg_set_capture_only", C.c_int, C.c_int)
 _sig("skg_spawn_pcg64", C.c_int, u64, P(C.c_char_p), C.c_int, P(u64))
 _sig("skg_choice_noreplace", C.c_int, P(u64), C.c_int, C.c_uint32, i64, i64, P(i64))
 _sig("skg_iteration_inputs", C.c_int, u64, i64, i64, i64, P(i64), i64, i64, P(i64), P(i64), P(u64))
+_sig("skg_group_inputs", C.c_int, u64, C.c_int, P(i64), P(i64), P(i32), P(u64), P(i64), i64, P(i64),
+     P(i64), P(u64), C.c_int)
 _sig("skg_ctx_create", C.c_int, C.c_int, i64, i64, P(i64), P(i32), P(dbl), i32, P(i32), P(vp))
 _sig("skg_ctx_destroy", C.c_int, vp)
 _sig("skg_ctx_set_features", C.c_int, vp, C.c_int, i64, i64, vp)
@@ -110,7 +112,7 @@ _sig("skg_debug_fr_trace", C.c_int, C.c_int, P(C.c_ulonglong))
 EXPORTED = [
     "skg_abi_version", "skg_last_error", "skg_kernel_launches", "skg_device_count",
     "skg_profile_start", "skg_profile_stop", "skg_profile_table", "skg_set_capture_only",
-    "skg_spawn_pcg64", "skg_choice_noreplace", "skg_iteration_inputs", "skg_ctx_create",
+    "skg_spawn_pcg64", "skg_choice_noreplace", "skg_iteration_inputs", "skg_group_inputs", "skg_ctx_create",
     "skg_ctx_destroy", "skg_ctx_set_features", "skg_ctx_set_features_bits", "skg_ctx_set_feature_map", "skg_ctx_feature_ptr", "skg_ctx_shard_upload",
     "skg_ctx_set_labels", "skg_ctx_set_multilabels", "skg_gcn_set_loss", "skg_ctx_set_owner", "skg_ctx_info", "skg_plans_ledger_add", "skg_plans_sticky_error", "skg_ipc_handle", "skg_ipc_open", "skg_ipc_close",
     "skg_plans_create", "skg_plans_destroy", "skg_ladies_sample", "skg_ladies_sample_device",

@@ -1,5 +1,9 @@
 // extern "C" boundary (include/skewgcn_b200.h): graph store, plan arenas, orchestration.
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <thread>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -572,6 +576,107 @@ extern "C" int skg_iteration_inputs(uint64_t master_seed, int64_t epoch, int64_t
   plan_state[1] = (uint64_t)p.state;
   plan_state[2] = (uint64_t)(p.inc >> 64);
   plan_state[3] = (uint64_t)p.inc;
+  return SKG_OK;
+}
+
+// Persistent host thread pool for the per-iteration host work of whole look-ahead groups.
+namespace {
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool p;
+    return p;
+  }
+  // run fn(i) for i in [0, n) on up to `threads` workers (the caller takes part)
+  void run(int n, int threads, const std::function<void(int)>& fn) {
+    std::lock_guard<std::mutex> one(call_);  // one group at a time
+    threads = std::max(1, std::min(threads, n));
+    if (threads == 1) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    std::unique_lock<std::mutex> lk(m_);
+    ensure(threads - 1);
+    job_ = &fn;
+    n_ = n;
+    next_.store(0);
+    want_ = threads - 1;
+    busy_ = 0;
+    ++gen_;
+    cv_.notify_all();
+    lk.unlock();
+    drain();
+    lk.lock();
+    done_.wait(lk, [&] { return busy_ == 0 && want_ == 0; });
+    job_ = nullptr;
+  }
+  ~HostPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+
+ private:
+  void ensure(int k) {
+    while ((int)th_.size() < k) th_.emplace_back([this] { loop(); });
+  }
+  void drain() {
+    for (int i = next_.fetch_add(1); i < n_; i = next_.fetch_add(1)) (*job_)(i);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    std::unique_lock<std::mutex> lk(m_);
+    for (;;) {
+      cv_.wait(lk, [&] { return stop_ || (gen_ != seen && want_ > 0); });
+      if (stop_) return;
+      seen = gen_;
+      --want_;
+      ++busy_;
+      lk.unlock();
+      drain();
+      lk.lock();
+      --busy_;
+      if (busy_ == 0 && want_ == 0) done_.notify_all();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex m_, call_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  int n_ = 0, want_ = 0, busy_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+  std::atomic<int> next_{0};
+};
+}  // namespace
+
+// skg_iteration_inputs for n worker-iterations at once (a Trainer look-ahead group): item i
+// = (epochs[i], its[i], workers[i]) over the worker's training nodes train_ptrs[i] (length
+// train_lens[i]); its batch is packed at out_batch[out_off[i] .. out_off[i + 1]) and its
+// plan state at plan_states[4 i ..].  Items run on up to n_threads host threads; the
+// results are those of n sequential skg_iteration_inputs calls.
+extern "C" int skg_group_inputs(uint64_t master_seed, int n, const int64_t* epochs, const int64_t* its,
+                                const int32_t* workers, const uint64_t* train_ptrs,
+                                const int64_t* train_lens, int64_t batch_size, int64_t* out_batch,
+                                int64_t* out_off, uint64_t* plan_states, int n_threads) {
+  ARG(n >= 0 && batch_size >= 1 && epochs && its && workers && train_ptrs && train_lens && out_batch &&
+          out_off && plan_states,
+      "bad group inputs");
+  for (int i = 0; i < n; ++i) ARG(train_lens[i] > 0, "worker has no training nodes");
+  std::vector<int64_t> tmp((size_t)n * batch_size), len(n);
+  HostPool::get().run(n, n_threads, [&](int i) {
+    skg_iteration_inputs(master_seed, epochs[i], its[i], workers[i],
+                         reinterpret_cast<const int64_t*>(train_ptrs[i]), train_lens[i], batch_size,
+                         tmp.data() + (size_t)i * batch_size, &len[i], plan_states + 4 * (size_t)i);
+  });
+  out_off[0] = 0;
+  for (int i = 0; i < n; ++i) {
+    std::memcpy(out_batch + out_off[i], tmp.data() + (size_t)i * batch_size, sizeof(int64_t) * len[i]);
+    out_off[i + 1] = out_off[i] + len[i];
+  }
   return SKG_OK;
 }
 

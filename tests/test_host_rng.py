@@ -67,3 +67,35 @@ def test_iteration_inputs_match_reference_loop(n_train, bs):
                                        ptr(out, C.c_int64), C.byref(n), ptr(st, C.c_uint64)))
         np.testing.assert_array_equal(out[: n.value], exp)
         np.testing.assert_array_equal(st, exp_state)
+
+
+def test_group_inputs_equal_per_iteration_calls():
+    """skg_group_inputs (a look-ahead group's host work on a thread pool) == the
+    per-iteration skg_iteration_inputs calls, item by item."""
+    import ctypes as C
+    from paper_2101_07706_b200._native import check, lib, ptr
+    rng = np.random.default_rng(3)
+    tws = [np.sort(rng.choice(50_000, int(rng.integers(300, 4000)), replace=False)).astype(np.int64)
+           for _ in range(6)]
+    n = 18
+    ep = rng.integers(0, 3, n).astype(np.int64)
+    its = rng.integers(0, 50, n).astype(np.int64)
+    ws = rng.integers(0, 6, n).astype(np.int32)
+    ptrs = np.array([tws[w].ctypes.data for w in ws], dtype=np.uint64)
+    lens = np.array([len(tws[w]) for w in ws], dtype=np.int64)
+    bs = 512
+    bids = np.zeros(n * bs, dtype=np.int64)
+    boff = np.zeros(n + 1, dtype=np.int64)
+    st = np.zeros((n, 4), dtype=np.uint64)
+    check(lib.skg_group_inputs(11, n, ptr(ep, C.c_int64), ptr(its, C.c_int64), ptr(ws, C.c_int32),
+                               ptr(ptrs, C.c_uint64), ptr(lens, C.c_int64), bs, ptr(bids, C.c_int64),
+                               ptr(boff, C.c_int64), ptr(st, C.c_uint64), 4))
+    b1 = np.zeros(bs, dtype=np.int64)
+    s1 = np.zeros(4, dtype=np.uint64)
+    ln = C.c_int64()
+    for i in range(n):
+        check(lib.skg_iteration_inputs(11, int(ep[i]), int(its[i]), int(ws[i]), ptr(tws[ws[i]], C.c_int64),
+                                       len(tws[ws[i]]), bs, ptr(b1, C.c_int64), C.byref(ln),
+                                       ptr(s1, C.c_uint64)))
+        np.testing.assert_array_equal(bids[boff[i]:boff[i + 1]], b1[:ln.value])
+        np.testing.assert_array_equal(st[i], s1)
