@@ -639,7 +639,7 @@ def run_ours(args):
                                    "gcn_fwd_bwd_step": round(float(np.median(comp_ms)), 4)},
             "roofline": {"bound": top["bound"], "kernel": top["kernel"],
                          "achieved": top["achieved"], "peak": top["peak"], "unit": top["unit"],
-                         "frac": top["frac"], **ncu_traffic(top["kernel"]),
+                         "frac": top["frac"], **ncu_traffic(top["kernel"], args.shape),
                          **{k_: top[k_] for k_ in ("frac_of_3xtf32_peak", "peak_note") if k_ in top},
                          "per_launch": top["per_launch"], "avg_launch_us": top["avg_us"],
                          "share_of_step": top["share"],
@@ -775,17 +775,19 @@ def kernel_table(lib, steps_fn, W, K, stats, tr, T, peaks, saint, budget):
     return out, all_ms
 
 
-def ncu_traffic(kernel_label):
+def ncu_traffic(kernel_label, shape="reddit"):
     """DRAM bytes per launch of the roofline kernel from the committed ncu --set full
     extract (profiles/ncu_traffic.json, tools/ncu_traffic.py; cold-cache replay, so an upper
-    bound on the in-step traffic); null when the kernel was not captured."""
+    bound on the in-step traffic); null when the kernel was not captured on this shape
+    (entries without a "shape" were captured on the default Reddit workload)."""
     path = ROOT / "profiles" / "ncu_traffic.json"
     base = kernel_label.split(" ")[0].split("<")[0]
     try:
         table = json.loads(path.read_text())
     except (OSError, ValueError):
         return {"traffic": None}
-    hits = [k for k in table if k == base or k.startswith(base + "_")]
+    hits = [k for k in table if (k == base or k.startswith(base + "_"))
+            and table[k].get("shape", "reddit") == shape]
     if not hits:
         return {"traffic": None}
     t = table[hits[0]]
