@@ -531,12 +531,17 @@ class Trainer:
     (training.py:488-493), so the plans of ``ahead`` future iterations are sampled by one
     batched launch sequence (``sample_group``) and consumed one iteration at a time by
     ``compute`` + ``reduce_and_step``; results are identical to sampling them one by one.
+
+    ``deterministic`` (several ranks only): instead of an all-reduce of per-rank gradient
+    sums, every worker's gradient is all-gathered and summed from zero in worker order, the
+    reference's own order (training.py:500-504), so the run is bit-identical to the
+    single-process one (for unsplit contractions; SURVEY §8 A19's ordered mode).
     """
 
     def __init__(self, g, partition, model, cfg, *, batch_size, lr, mode, seed,
                  sampler="ladies", subgraph_size=None, optimizer="sgd", dtype=None,
                  epochs=1, workers=None, ahead=1, shard_features=None, streams=1,
-                 loss="auto", pos_weight=50.0):
+                 loss="auto", pos_weight=50.0, deterministic=False):
         torch = _torch()
         if g.features is None or g.labels is None or g.train_mask is None:
             raise ValueError("training needs features, labels and masks")
@@ -622,6 +627,21 @@ class Trainer:
             o += w.size
         self.wp = np.array([v.data_ptr() for v in self.wviews], dtype=np.uint64)
         self.gp = np.array([v.data_ptr() for v in self.gviews], dtype=np.uint64)
+        self.deterministic = bool(deterministic) and self.world > 1
+        if self.deterministic:
+            # per-worker gradients (rows padded to the largest rank's worker count)
+            counts = [len(assign_workers(self.active, r, self.world)) for r in range(self.world)]
+            self._wcap = max(counts)
+            self._wcounts = counts
+            self.wgrads = torch.zeros((self._wcap, self.n_params), dtype=td, device="cuda")
+            self._wgp = []
+            for i in range(self._wcap):
+                o, ptrs = 0, []
+                for w in model.weights:
+                    ptrs.append(self.wgrads[i, o:o + w.size].data_ptr())
+                    o += w.size
+                self._wgp.append(np.array(ptrs, dtype=np.uint64))
+            self._gathered = torch.zeros((self.world * self._wcap, self.n_params), dtype=td, device="cuda")
         if optimizer == "adam":
             self.m = torch.zeros_like(self.wflat)
             self.v = torch.zeros_like(self.wflat)
@@ -787,10 +807,17 @@ class Trainer:
         if self.n_my:
             ps, gcn = self.bufs[buf]
             s0 = group * self.n_my
-            # all of this rank's workers in one batched pass; gradients summed in worker order
-            check(lib.skg_gcn_step_batch(gcn, s0, self.n_my, ptr(self.wp, C.c_uint64),
-                                         ptr(self.gp, C.c_uint64), 0,
-                                         self.losses[it % self.per_epoch].data_ptr(), self.stream))
+            if self.deterministic:  # every worker's gradient kept apart (ordered reduction)
+                lrow = self.losses[it % self.per_epoch]
+                for i in range(self.n_my):
+                    check(lib.skg_gcn_step_batch(gcn, s0 + i, 1, ptr(self.wp, C.c_uint64),
+                                                 ptr(self._wgp[i], C.c_uint64), 0,
+                                                 lrow[i:].data_ptr(), self.stream))
+            else:
+                # all of this rank's workers in one batched pass; gradients summed in worker order
+                check(lib.skg_gcn_step_batch(gcn, s0, self.n_my, ptr(self.wp, C.c_uint64),
+                                             ptr(self.gp, C.c_uint64), 0,
+                                             self.losses[it % self.per_epoch].data_ptr(), self.stream))
             check(lib.skg_plans_ledger_add(ps.h, s0, self.n_my,
                                            self.ledger[epoch % self.ledger.shape[0]].data_ptr(),
                                            self.stream))
@@ -798,7 +825,16 @@ class Trainer:
             check(lib.skg_zero(self.dtc, self.gflat.data_ptr(), self.n_params, self.stream))
 
     def reduce_and_step(self):
-        if self.world > 1:
+        if self.deterministic:
+            # all ranks' per-worker gradients, summed from zero in worker order (ranks hold
+            # contiguous worker blocks, so rank-major rows are worker order)
+            self.dist.all_gather(list(self._gathered.view(self.world, self._wcap, -1).unbind(0)),
+                                 self.wgrads)
+            self.gflat.zero_()
+            for r in range(self.world):
+                for i in range(self._wcounts[r]):
+                    self.gflat.add_(self._gathered[r * self._wcap + i])
+        elif self.world > 1:
             self.dist.all_reduce(self.gflat)
         contrib = float(len(self.active))
         if self.optimizer == "sgd":
@@ -915,7 +951,7 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
                       epochs: int, batch_size: int, lr: float, mode: str, seed: int,
                       sampler: str = "ladies", subgraph_size: int | None = None,
                       optimizer: str = "sgd", ahead: int = 3, streams: int = 2,
-                      pos_weight: float = 50.0) -> tuple:
+                      pos_weight: float = 50.0, deterministic: bool = False) -> tuple:
     """Data-parallel training with per-iteration gradient averaging (training.py:430-518).
 
     Single process: all workers run on this GPU.  Under torch.distributed (one process
@@ -930,17 +966,18 @@ def train_distributed(g: WeightedGraph, partition: Partition, model: GcnModel, c
     with torch.cuda.stream(hp):
         out = _train_distributed(g, partition, model, cfg, epochs=epochs, batch_size=batch_size, lr=lr,
                                  mode=mode, seed=seed, sampler=sampler, subgraph_size=subgraph_size,
-                                 optimizer=optimizer, ahead=ahead, streams=streams, pos_weight=pos_weight)
+                                 optimizer=optimizer, ahead=ahead, streams=streams, pos_weight=pos_weight,
+                                 deterministic=deterministic)
     torch.cuda.current_stream().wait_stream(hp)
     return out
 
 
 def _train_distributed(g, partition, model, cfg, *, epochs, batch_size, lr, mode, seed, sampler,
-                       subgraph_size, optimizer, ahead, streams, pos_weight):
+                       subgraph_size, optimizer, ahead, streams, pos_weight, deterministic):
     torch = _torch()
     tr = Trainer(g, partition, model, cfg, batch_size=batch_size, lr=lr, mode=mode, seed=seed,
                  sampler=sampler, subgraph_size=subgraph_size, optimizer=optimizer, epochs=epochs,
-                 ahead=ahead, streams=streams, pos_weight=pos_weight)
+                 ahead=ahead, streams=streams, pos_weight=pos_weight, deterministic=deterministic)
     k, L = tr.k, tr.L
     metrics = Metrics()
     val_nodes = np.flatnonzero(g.val_mask) if g.val_mask is not None else np.empty(0, dtype=np.int64)

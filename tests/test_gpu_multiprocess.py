@@ -59,3 +59,44 @@ def test_two_process_training_equals_single_process(tmp_path):
     np.testing.assert_allclose([r[2] for r in rows], [r[2] for r in rows1], rtol=1e-10)
     for a, b in zip(weights, weights1):
         np.testing.assert_allclose(a, b, rtol=1e-9, atol=1e-12)
+
+
+def _rank_main_det(rank, world, port, out):
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    P, g, part = _setup()
+    P.set_compute_dtype("float32")
+    model = P.init_model([16, 12, 12, 3], 4)
+    metrics, ledger = P.train_distributed(g, part, model, P.SamplerConfig(budget=64, skew_constant=8.0,
+                                                                          mode="skewed"),
+                                          epochs=2, batch_size=48, lr=0.2, mode="skewed", seed=3,
+                                          deterministic=True)
+    if rank == 0:
+        Path(out).write_bytes(pickle.dumps(([(r.epoch, r.worker, r.loss) for r in metrics.rows],
+                                            ledger.counts, model.weights)))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_process_deterministic_mode_is_bit_identical(tmp_path):
+    """deterministic=True: per-worker gradients all-gathered and summed in worker order, so
+    the 2-process fp32 run equals the single-process one bit for bit (weights and losses)."""
+    import torch.multiprocessing as mp
+    out = tmp_path / "r0.pkl"
+    mp.start_processes(_rank_main_det, args=(2, 29541, str(out)), nprocs=2, join=True, start_method="spawn")
+    rows, ledger, weights = pickle.loads(out.read_bytes())
+    P, g, part = _setup()
+    P.set_compute_dtype("float32")
+    model = P.init_model([16, 12, 12, 3], 4)
+    metrics, ledger1 = P.train_distributed(g, part, model, P.SamplerConfig(budget=64, skew_constant=8.0,
+                                                                           mode="skewed"),
+                                           epochs=2, batch_size=48, lr=0.2, mode="skewed", seed=3)
+    P.set_compute_dtype("float64")
+    assert np.array_equal(ledger, ledger1.counts)
+    assert rows == [(r.epoch, r.worker, r.loss) for r in metrics.rows]
+    for a, b in zip(weights, model.weights):
+        assert np.array_equal(a, b)
