@@ -415,7 +415,7 @@ def run_ours(args):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     fr_trace = os.environ.get("SKG_FR_TRACE")  # diagnostic: range-expand CTA timeline
     if fr_trace:
-        lib.skg_debug_fr_trace(1, None)
+        lib.skg_debug_fr_trace(1 + int(os.environ.get("SKG_FR_TRACE_THREAD", "0")), None)
     with ClockSampler(local) as clk:
         barrier()
         ev0.record(stream)
@@ -438,7 +438,7 @@ def run_ours(args):
     launches = P.kernel_launches() - launches0
     ms = ev0.elapsed_time(ev1)
     if fr_trace:
-        buf = (C.c_ulonglong * (8 * 32 * 9))()
+        buf = (C.c_ulonglong * (8 * 32 * 11))()
         lib.skg_debug_fr_trace(0, buf)
         with open(fr_trace, "w") as fh:
             json.dump(list(buf), fh)
