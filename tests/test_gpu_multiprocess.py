@@ -100,3 +100,54 @@ def test_two_process_deterministic_mode_is_bit_identical(tmp_path):
     assert rows == [(r.epoch, r.worker, r.loss) for r in metrics.rows]
     for a, b in zip(weights, model.weights):
         assert np.array_equal(a, b)
+
+
+def _binary_setup():
+    P, g, part = _setup()
+    rng = np.random.default_rng(5)
+    g.features = (rng.random((g.n_nodes, 256)) < 0.05).astype(np.float64)  # packed on upload
+    return P, g, part
+
+
+def _train_bits(P, g, part):
+    P.set_compute_dtype("float64")
+    model = P.init_model([256, 12, 12, 3], 4)
+    metrics, ledger = P.train_distributed(g, part, model, P.SamplerConfig(budget=64, skew_constant=8.0,
+                                                                          mode="skewed"),
+                                          epochs=1, batch_size=48, lr=0.2, mode="skewed", seed=3,
+                                          deterministic=True)
+    return [(r.epoch, r.worker, r.loss) for r in metrics.rows], ledger.counts, model.weights
+
+
+def _rank_main_bits(rank, world, port, out):
+    sys.path.insert(0, str(ROOT))
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    P, g, part = _binary_setup()
+    res = _train_bits(P, g, part)
+    from paper_2101_07706_b200 import _device as D
+    res = res + (bool(D.device_graph(g).xbits),)
+    if rank == 0:
+        Path(out).write_bytes(pickle.dumps(res))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_process_bit_packed_feature_shards(tmp_path):
+    """0/1 features are packed on upload, each rank's shard is uploaded packed and the peer
+    shards are read bit-packed through CUDA IPC by the fused layer-0 SpMM; with the ordered
+    reduction the 2-process run equals the single-process one bit for bit."""
+    import torch.multiprocessing as mp
+    out = tmp_path / "r0.pkl"
+    mp.start_processes(_rank_main_bits, args=(2, 29547, str(out)), nprocs=2, join=True, start_method="spawn")
+    rows, ledger, weights, packed = pickle.loads(out.read_bytes())
+    assert packed
+    P, g, part = _binary_setup()
+    rows1, ledger1, weights1 = _train_bits(P, g, part)
+    assert np.array_equal(ledger, ledger1)
+    assert rows == rows1
+    for a, b in zip(weights, weights1):
+        assert np.array_equal(a, b)
