@@ -4,6 +4,8 @@
 #include <condition_variable>
 #include <functional>
 #include <thread>
+
+#include <unistd.h>
 #include <cstddef>
 #include <cstdio>
 #include <cstdlib>
@@ -591,6 +593,8 @@ class HostPool {
   void run(int n, int threads, const std::function<void(int)>& fn) {
     std::lock_guard<std::mutex> one(call_);  // one group at a time
     threads = std::max(1, std::min(threads, n));
+    // a forked child has none of the parent's workers: run inline there
+    if (!th_.empty() && getpid() != pid_) threads = 1;
     if (threads == 1) {
       for (int i = 0; i < n; ++i) fn(i);
       return;
@@ -611,6 +615,10 @@ class HostPool {
     job_ = nullptr;
   }
   ~HostPool() {
+    if (!th_.empty() && getpid() != pid_) {  // forked child: the threads are not ours
+      for (auto& t : th_) t.detach();
+      return;
+    }
     {
       std::lock_guard<std::mutex> lk(m_);
       stop_ = true;
@@ -621,6 +629,7 @@ class HostPool {
 
  private:
   void ensure(int k) {
+    if (th_.empty()) pid_ = getpid();
     while ((int)th_.size() < k) th_.emplace_back([this] { loop(); });
   }
   void drain() {
@@ -649,6 +658,7 @@ class HostPool {
   int n_ = 0, want_ = 0, busy_ = 0;
   uint64_t gen_ = 0;
   bool stop_ = false;
+  pid_t pid_ = 0;
   std::atomic<int> next_{0};
 };
 }  // namespace
