@@ -233,12 +233,15 @@ def bench_config(args, n_nodes, nnz, feat_dim):
     """The workload description both arms print (identical dicts: same_config)."""
     l2_mb = 126
     cols_mb = nnz * 4 / 1e6
-    feat_mb = n_nodes * feat_dim * 4 / 1e6
+    packed = args.shape.startswith("youtube")  # build_workload stores these rows bit-packed
+    feat_mb = n_nodes * (((feat_dim + 31) // 32) * 4 if packed else feat_dim * 4) / 1e6
+    feat = "bit-packed features" if packed else "fp32 features"
+    touch = ("every plan touches ~2/3 of the nodes" if args.shape.startswith("reddit")
+             else "each step samples fresh random batches")
     return {"workload": workload_name(args), "n_nodes": int(n_nodes), "nnz": int(nnz),
             "feature_dim": int(feat_dim), "workers": args.workers,
             "l2": (f"inputs > L2: {cols_mb:.0f} MB of CSR columns and {feat_mb:.0f} MB of "
-                   f"features against a {l2_mb} MB L2, every plan touches ~2/3 of the nodes; "
-                   "no flush between steps")}
+                   f"{feat} against a {l2_mb} MB L2, {touch}; no flush between steps")}
 
 
 def build_workload(args, device):
