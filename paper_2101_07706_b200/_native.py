@@ -107,6 +107,7 @@ _sig("skg_debug_gemm", C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c
      P(C.c_float), P(C.c_float))
 _sig("skg_set_gemm_mode", C.c_int, C.c_int)
 _sig("skg_debug_fr_trace", C.c_int, C.c_int, P(C.c_ulonglong))
+_sig("skg_debug_norm_w", C.c_int, P(dbl), i64, P(dbl), P(dbl))
 
 # every symbol the public header declares (checked by tests/test_native_abi.py)
 EXPORTED = [

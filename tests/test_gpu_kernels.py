@@ -56,3 +56,27 @@ def test_gemm_3xtf32_beats_1xtf32():
     e1 = np.abs(_gemm(1, False, False, a, b, M, N, K) - ref).max()
     e3 = np.abs(_gemm(3, False, False, a, b, M, N, K) - ref).max()
     assert e3 * 50 < e1
+
+
+def test_norm_w_fast_paths_bit_identical():
+    """The sampler's branch-free sqrt / reciprocal (sampler.cu sqrt_rn_pos, rcp_rn_pos) give
+    the bits of __dsqrt_rn / __drcp_rn on the degree products w_ij = 1/sqrt(d_i d_j) is
+    computed from (graph.py:180-182): every product up to 2^24, every d_i d_j with
+    d <= 3000, and random products of degrees up to 2^31 and doubles up to 2^62."""
+    from paper_2101_07706_b200._native import lib, ptr
+    r = np.random.default_rng(7)
+    d = np.arange(1, 3001, dtype=np.float64)
+    parts = [np.arange(1, 1 << 24, dtype=np.float64),
+             np.unique(np.outer(d, d).ravel()),
+             (r.integers(1, 1 << 31, 4_000_000).astype(np.float64)
+              * r.integers(1, 1 << 31, 4_000_000).astype(np.float64)),
+             np.exp2(r.uniform(0, 62, 4_000_000))]
+    p = np.ascontiguousarray(np.concatenate(parts))
+    fast = np.empty_like(p)
+    ref = np.empty_like(p)
+    dbl = C.c_double
+    assert lib.skg_debug_norm_w(ptr(p, dbl), len(p), ptr(fast, dbl), ptr(ref, dbl)) == 0
+    bad = np.flatnonzero(fast.view(np.uint64) != ref.view(np.uint64))
+    assert bad.size == 0, (bad.size, p[bad[:5]], fast[bad[:5]], ref[bad[:5]])
+    # and both are the correctly rounded 1 / sqrt(p) numpy computes (spot check)
+    np.testing.assert_array_equal(ref[:1 << 20], 1.0 / np.sqrt(p[:1 << 20]))
