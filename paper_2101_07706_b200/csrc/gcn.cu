@@ -413,13 +413,44 @@ template <typename T>
 __global__ void k_reduce_slots(const T* parts, int64_t pstride, int n, int64_t rows, int64_t cols,
                                int64_t ldp, T* C, int64_t ldc, int accumulate) {
   SKG_PDL_PROLOGUE();
-  const int64_t total = rows * cols;
+  // VW consecutive columns per thread (VW = 4 when every row and part is 16-byte aligned);
+  // the parts' loads of a run of 8 slots are all issued before the in-order adds, so the
+  // sum (C or 0, then slot 0, 1, ...) keeps its order and the loads overlap
+  const bool vec = sizeof(T) == 4 && cols % 4 == 0 && ldp % 4 == 0 && ldc % 4 == 0 && pstride % 4 == 0 &&
+                   (reinterpret_cast<uintptr_t>(parts) & 15) == 0 && (reinterpret_cast<uintptr_t>(C) & 15) == 0;
+  const int vw = vec ? 4 : 1;
+  const int64_t cv = cols / vw;
+  const int64_t total = rows * cv;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / cols, c = i % cols;
-    T s = accumulate ? C[r * ldc + c] : T(0);
-    for (int z = 0; z < n; ++z) s += parts[z * pstride + r * ldp + c];
-    C[r * ldc + c] = s;
+    const int64_t r = i / cv, c = (i - r * cv) * vw;
+    if (vec) {
+      float4 s = accumulate ? *reinterpret_cast<const float4*>(C + r * ldc + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int z0 = 0; z0 < n; z0 += 8) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (z0 + u < n) v[u] = *reinterpret_cast<const float4*>(parts + (z0 + u) * pstride + r * ldp + c);
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (z0 + u < n) {
+            s.x += v[u].x; s.y += v[u].y; s.z += v[u].z; s.w += v[u].w;
+          }
+      }
+      *reinterpret_cast<float4*>(C + r * ldc + c) = s;
+    } else {
+      T s = accumulate ? C[r * ldc + c] : T(0);
+      for (int z0 = 0; z0 < n; z0 += 8) {
+        T v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (z0 + u < n) v[u] = parts[(z0 + u) * pstride + r * ldp + c];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (z0 + u < n) s += v[u];
+      }
+      C[r * ldc + c] = s;
+    }
   }
 }
 
