@@ -131,6 +131,7 @@ struct TcMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
   CUtensorMap c;  // output boxes {32 columns, 128 rows, 1 block} for the TMA-store epilogue
   int c_tma;      // 1: the epilogue stages the tile in shared memory and stores it by TMA
+  int early;      // 1: stage 0's TMA loads are issued before the setup sync (k_gemm_tc)
 };
 
 // debug timeline of CTA (0, 0, 0) (globaltimer ns): [0] start, [1] after setup,
@@ -151,7 +152,6 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
     k_gemm_tc(const __grid_constant__ TcMaps maps, int Mfix, int N, int Kfix,
               const int32_t* const* dM, const int32_t* const* dK, int a_slots, int b_slots,
               Act<float> C, int accumulate, int ks) {
-  SKG_PDL_PROLOGUE();
   using namespace tc;
   using CF = Cfg<BN, MODE>;
   constexpr bool SPLIT = MODE == 3;
@@ -183,6 +183,37 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
                  "n"(TCOLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // under PDL the CTA may start while the previous grid of the stream drains: TMEM is
+  // allocated above, every global access waits here
+  SKG_PDL_WAIT();
+  const int za = a_slots > 1 ? z : 0, zb = b_slots > 1 ? z : 0;
+  // TMA loads of K chunk kc into its ring stage (the producer thread only)
+  auto load_stage = [&](int kc) {
+    const int s = kc % STAGES;
+    uint8_t* st = smem + s * CF::STAGE;
+    mbar_expect_tx(&full_bar[s], (uint32_t)CF::STAGE);
+    if (tr && kc < 32) g_tc_trace[34 + kc] = gtimer();
+    const int k0 = (kc0 + kc) * BK;
+#pragma unroll
+    for (int part = 0; part < CF::PARTS; ++part) {
+      uint8_t* sa = st + part * (CF::A_BYTES + CF::B_BYTES);
+      uint8_t* sb = sa + CF::A_BYTES;
+      const CUtensorMap* ma = part ? &maps.a_lo : &maps.a_hi;
+      const CUtensorMap* mb = part ? &maps.b_lo : &maps.b_hi;
+      if (A_MN) {
+#pragma unroll
+        for (int i = 0; i < BM / 32; ++i) tma3(sa + i * 4096, ma, m0 + 32 * i, k0, za, &full_bar[s]);
+      } else {
+        tma3(sa, ma, k0, m0, za, &full_bar[s]);
+      }
+      if (B_MN) {
+#pragma unroll
+        for (int i = 0; i < BN / 32; ++i) tma3(sb + i * 4096, mb, n0 + 32 * i, k0, zb, &full_bar[s]);
+      } else {
+        tma3(sb, mb, k0, n0, zb, &full_bar[s]);
+      }
+    }
+  };
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full_bar[s], 1);   // producer's expect_tx arrival (+ TMA bytes)
@@ -190,6 +221,8 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
     }
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
+    // the first chunk's loads fly while TMEM is allocated and the CTA synchronises
+    if (maps.early && nk > 0) load_stage(0);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -200,33 +233,10 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      const int za = a_slots > 1 ? z : 0, zb = b_slots > 1 ? z : 0;
-      for (int kc = 0; kc < nk; ++kc) {
+      for (int kc = maps.early ? 1 : 0; kc < nk; ++kc) {
         const int s = kc % STAGES;
         if (kc >= STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((kc / STAGES) - 1) & 1));
-        uint8_t* st = smem + s * CF::STAGE;
-        mbar_expect_tx(&full_bar[s], (uint32_t)CF::STAGE);
-        if (tr && kc < 32) g_tc_trace[34 + kc] = gtimer();
-        const int k0 = (kc0 + kc) * BK;
-#pragma unroll
-        for (int part = 0; part < CF::PARTS; ++part) {
-          uint8_t* sa = st + part * (CF::A_BYTES + CF::B_BYTES);
-          uint8_t* sb = sa + CF::A_BYTES;
-          const CUtensorMap* ma = part ? &maps.a_lo : &maps.a_hi;
-          const CUtensorMap* mb = part ? &maps.b_lo : &maps.b_hi;
-          if (A_MN) {
-#pragma unroll
-            for (int i = 0; i < BM / 32; ++i) tma3(sa + i * 4096, ma, m0 + 32 * i, k0, za, &full_bar[s]);
-          } else {
-            tma3(sa, ma, k0, m0, za, &full_bar[s]);
-          }
-          if (B_MN) {
-#pragma unroll
-            for (int i = 0; i < BN / 32; ++i) tma3(sb + i * 4096, mb, n0 + 32 * i, k0, zb, &full_bar[s]);
-          } else {
-            tma3(sb, mb, k0, n0, zb, &full_bar[s]);
-          }
-        }
+        load_stage(kc);
       }
     }
   } else if (warp == 1) {
@@ -266,6 +276,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   } else {
     // ---------------- epilogue: TMEM lane quarter (warp % 4), all BN columns
     mbar_wait(&done_bar, 0u);
+    if (threadIdx.x == 64) SKG_PDL_TRIGGER();  // the next grid may launch during the epilogue
     if (tr && threadIdx.x == 64) g_tc_trace[66] = gtimer();
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int lg = warp & 3;
@@ -697,6 +708,8 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
   rc = op_maps(B, !TB, N, K, BN, n, MODE == 3, &maps.b_hi, &maps.b_lo);
   if (rc) return rc;
   maps.c_tma = 0;
+  static const int early = getenv("SKG_GEMM_EARLY") ? atoi(getenv("SKG_GEMM_EARLY")) : 1;
+  maps.early = early;
   const int as = A.stride ? n : 1, bs = B.stride ? n : 1;
   const int tn = (N + BN - 1) / BN, tm = (M + tc::BM - 1) / tc::BM;
   const long long tiles = (long long)tn * tm * n * ks;

@@ -65,3 +65,7 @@ inline void launch_k(const char* name, cudaStream_t st, dim3 grid, dim3 block, s
 // the previous one (no-ops when launched without PDL).
 #define SKG_PDL_PROLOGUE() \
   asm volatile("griddepcontrol.launch_dependents;\n\tgriddepcontrol.wait;" ::: "memory")
+// Split form for kernels that trigger their dependents late (k_gemm_tc: once its accumulator
+// is complete, so waiting dependents never hold SMs through its main loop)
+#define SKG_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+#define SKG_PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
