@@ -93,7 +93,7 @@ __device__ __forceinline__ void store_split(const Vec4<double>&, double*, double
 template <typename T, bool TRANS, bool RELU>
 __global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, T* out_lo,
                          int max_rows, int64_t width) {
-  SKG_PDL_PROLOGUE();
+  SKG_PDL_WAIT();  // dependents are triggered at the end (GEMM CTAs must not wait on SMs)
   const LayerDesc d = lds[blockIdx.y];
   const int rows = TRANS ? *d.cols : *d.rows;
   const int32_t* __restrict__ ip = TRANS ? d.tindptr : d.indptr;
@@ -146,6 +146,7 @@ __global__ void k_spmm_b(const LayerDesc* lds, Act<T> A, Act<T> H, Act<T> out, T
       }
     }
   }
+  SKG_PDL_TRIGGER();
 }
 
 template <typename T>
@@ -172,7 +173,7 @@ __device__ __forceinline__ Vec4<T> bits4(const uint32_t* row, int64_t c) {
 template <typename T, bool BITS>
 __global__ void k_spmm_in_b(FeatStore fs, const SlotDesc* sd, const LayerDesc* lds, Act<T> out,
                             T* out_lo, int max_rows, int64_t width) {
-  SKG_PDL_PROLOGUE();
+  SKG_PDL_WAIT();  // dependents are triggered at the end (GEMM CTAs must not wait on SMs)
   const LayerDesc d = lds[blockIdx.y];
   const int32_t* __restrict__ in_nodes = sd[blockIdx.y].in_nodes;
   const int rows = *d.rows;
@@ -223,6 +224,7 @@ __global__ void k_spmm_in_b(FeatStore fs, const SlotDesc* sd, const LayerDesc* l
       }
     }
   }
+  SKG_PDL_TRIGGER();
 }
 
 template <typename T>
