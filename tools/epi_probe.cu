@@ -95,6 +95,40 @@ __global__ void __launch_bounds__(128, 1) epi(const __grid_constant__ CUtensorMa
     }
     asm volatile("cp.async.bulk.commit_group;");
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+  } else if (mode == 4) {
+    // two boxes per step: four TMEM loads in flight per wait
+#pragma unroll 1
+    for (int b = 0; b < BN / 32; b += 2) {
+      uint32_t v[64];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[16 * h + 0]), "=r"(v[16 * h + 1]), "=r"(v[16 * h + 2]), "=r"(v[16 * h + 3]), "=r"(v[16 * h + 4]),
+              "=r"(v[16 * h + 5]), "=r"(v[16 * h + 6]), "=r"(v[16 * h + 7]), "=r"(v[16 * h + 8]), "=r"(v[16 * h + 9]),
+              "=r"(v[16 * h + 10]), "=r"(v[16 * h + 11]), "=r"(v[16 * h + 12]), "=r"(v[16 * h + 13]),
+              "=r"(v[16 * h + 14]), "=r"(v[16 * h + 15])
+            : "r"(trow + b * 32 + 16 * h));
+      asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb) {
+        uint8_t* box = sm + (b + bb) * (BM * 128) + row * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(box + ((c ^ (row & 7)) * 16)) =
+              make_uint4(v[32 * bb + 4 * c], v[32 * bb + 4 * c + 1], v[32 * bb + 4 * c + 2], v[32 * bb + 4 * c + 3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;");
+      asm volatile("bar.sync 1, 128;");
+      if (threadIdx.x == 0) {
+        for (int bb = 0; bb < 2; ++bb)
+          asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tc),
+                       "r"((b + bb) * 32), "r"(blockIdx.x * BM), "r"(su32(sm + (b + bb) * BM * 128))
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;");
+      }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
   } else if (mode == 2) {
     // per box: two TMEM loads in flight per wait, stage the box, then one thread issues its
     // TMA store while the next box is read from TMEM
@@ -183,7 +217,7 @@ int main() {
   if (r != CUDA_SUCCESS) printf("encode failed %d\n", (int)r);
   cudaFuncSetAttribute(epi, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
   std::vector<float> c(rows * BN);
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 5; ++mode) {
     for (int it = 0; it < 3; ++it) {
       cudaMemset(dC, 0, rows * BN * 4);
       epi<<<NCTA, 128, 80 * 1024>>>(tc, dC, mode, dcy);
@@ -201,7 +235,7 @@ int main() {
         mx = v > mx ? v : mx;
       }
       printf("%s  epilogue cycles mean %.0f max %lld  (%.2f us at 1.965 GHz)  bad %lld  (%s)\n",
-             mode == 3 ? "bulk copy per row  " : mode == 2 ? "TMA store per box  " : mode ? "TMA store via smem " : "row float4 stores  ", mean / NCTA, mx, mean / NCTA / 1965.0, bad,
+             mode == 4 ? "TMA store 2 boxes  " : mode == 3 ? "bulk copy per row  " : mode == 2 ? "TMA store per box  " : mode ? "TMA store via smem " : "row float4 stores  ", mean / NCTA, mx, mean / NCTA / 1965.0, bad,
              cudaGetErrorString(e));
       if (e != cudaSuccess) return 1;
     }
