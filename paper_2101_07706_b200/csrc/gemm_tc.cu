@@ -99,6 +99,15 @@ __device__ __forceinline__ void tma3(void* dst, const CUtensorMap* map, int c0, 
       : "memory");
 }
 
+__device__ __forceinline__ void tma4(void* dst, const CUtensorMap* map, int c0, int c1, int c2, int c3,
+                                     uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -132,6 +141,7 @@ struct TcMaps {
   CUtensorMap c;  // output boxes {32 columns, 128 rows, 1 block} for the TMA-store epilogue
   int c_tma;      // 1: the epilogue stages the tile in shared memory and stores it by TMA
   int early;      // 1: stage 0's TMA loads are issued before the setup sync (k_gemm_tc)
+  int a_blk, b_blk;  // 1: the MN-major operand's 32-wide blocks come in one 4D box (k_gemm_tc)
 };
 
 // debug timeline of CTA (0, 0, 0) (globaltimer ns): [0] start, [1] after setup,
@@ -200,13 +210,17 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
       uint8_t* sb = sa + CF::A_BYTES;
       const CUtensorMap* ma = part ? &maps.a_lo : &maps.a_hi;
       const CUtensorMap* mb = part ? &maps.b_lo : &maps.b_hi;
-      if (A_MN) {
+      if (A_MN && maps.a_blk) {
+        tma4(sa, ma, 0, k0, m0 / 32, za, &full_bar[s]);  // BM / 32 blocks of {32 mn, 32 k}, 4 KB apart
+      } else if (A_MN) {
 #pragma unroll
         for (int i = 0; i < BM / 32; ++i) tma3(sa + i * 4096, ma, m0 + 32 * i, k0, za, &full_bar[s]);
       } else {
         tma3(sa, ma, k0, m0, za, &full_bar[s]);
       }
-      if (B_MN) {
+      if (B_MN && maps.b_blk) {
+        tma4(sb, mb, 0, k0, n0 / 32, zb, &full_bar[s]);
+      } else if (B_MN) {
 #pragma unroll
         for (int i = 0; i < BN / 32; ++i) tma3(sb + i * 4096, mb, n0 + 32 * i, k0, zb, &full_bar[s]);
       } else {
@@ -611,7 +625,7 @@ std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
 // {32, box_outer, 1}, SWIZZLE_128B (K-major) or SWIZZLE_128B_ATOM_32B (MN-major), zero fill
 // out of bounds
 int get_map(const float* base, int64_t inner, int64_t outer, int64_t slots, int64_t ld, int64_t stride,
-            int box_outer, bool mn, CUtensorMap* out) {
+            int box_outer, int mn, CUtensorMap* out) {
   MapKey key;
   memset(&key, 0, sizeof(key));
   key.base = base;
@@ -639,15 +653,29 @@ int get_map(const float* base, int64_t inner, int64_t outer, int64_t slots, int6
     set_error("gemm operand not TMA-compatible (ld / base alignment)");
     return SKG_ERR_ARG;
   }
-  cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)std::max<int64_t>(slots, 1)};
-  cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)std::max<int64_t>(stride, ld * outer) * 4};
-  cuuint32_t box[3] = {32, (cuuint32_t)box_outer, 1};
-  cuuint32_t es[3] = {1, 1, 1};
   CUtensorMap m;
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r;
+  if (mn == 2) {
+    // MN-major operand as 4D {32 mn, k rows, inner / 32 blocks, slots}, box {32, 32 k,
+    // blk_count, 1}: one TMA lands blk_count {32 mn, 32 k} blocks 4 KB apart, the layout the
+    // per-block boxes produce (inner must be a multiple of 32: no partial block to zero-fill)
+    const int blk_count = (int)(box_outer >> 8), k_box = (int)(box_outer & 255);
+    cuuint64_t dims[4] = {32, (cuuint64_t)outer, (cuuint64_t)(inner / 32), (cuuint64_t)std::max<int64_t>(slots, 1)};
+    cuuint64_t strides[3] = {(cuuint64_t)ld * 4, 128, (cuuint64_t)std::max<int64_t>(stride, ld * outer) * 4};
+    cuuint32_t box[4] = {32, (cuuint32_t)k_box, (cuuint32_t)blk_count, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  } else {
+    cuuint64_t dims[3] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)std::max<int64_t>(slots, 1)};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 4, (cuuint64_t)std::max<int64_t>(stride, ld * outer) * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)box_outer, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, mn ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   if (r != CUDA_SUCCESS) {
     set_error("cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
     return SKG_ERR_CUDA;
@@ -660,19 +688,31 @@ int get_map(const float* base, int64_t inner, int64_t outer, int64_t slots, int6
 }
 
 // operand maps: K-major operands are boxed {32 k, rows}; MN-major {32 mn, 32 k}
+// (blk: an MN-major operand whose extent is a multiple of 32 gets the 4D block map, one TMA
+// per stage instead of rows_box / 32; *blk_out says which was built)
 int op_maps(const TcOp& op, bool mn, int64_t mn_extent, int64_t k_extent, int rows_box, int n,
-            bool split, CUtensorMap* hi, CUtensorMap* lo) {
+            bool split, CUtensorMap* hi, CUtensorMap* lo, bool blk = false, int* blk_out = nullptr) {
   const int64_t slots = op.stride ? n : 1;
   const int64_t inner = mn ? mn_extent : k_extent;
+  if (blk_out) *blk_out = 0;
+  if (mn && blk && mn_extent % 32 == 0) {
+    const int bo = ((rows_box / 32) << 8) | tc::BK;
+    if (get_map(op.hi, inner, op.rows_cap, slots, op.ld, op.stride, bo, 2, hi) == SKG_OK &&
+        (!split || (op.lo && get_map(op.lo, inner, op.rows_cap, slots, op.ld, op.stride, bo, 2, lo) == SKG_OK))) {
+      if (!split) *lo = *hi;
+      if (blk_out) *blk_out = 1;
+      return SKG_OK;
+    }
+  }
   const int box_outer = mn ? tc::BK : rows_box;
-  int rc = get_map(op.hi, inner, op.rows_cap, slots, op.ld, op.stride, box_outer, mn, hi);
+  int rc = get_map(op.hi, inner, op.rows_cap, slots, op.ld, op.stride, box_outer, mn ? 1 : 0, hi);
   if (rc) return rc;
   if (split) {
     if (!op.lo) {
       set_error("3xTF32 GEMM needs the lo operand");
       return SKG_ERR_ARG;
     }
-    rc = get_map(op.lo, inner, op.rows_cap, slots, op.ld, op.stride, box_outer, mn, lo);
+    rc = get_map(op.lo, inner, op.rows_cap, slots, op.ld, op.stride, box_outer, mn ? 1 : 0, lo);
     if (rc) return rc;
   } else {
     *lo = *hi;
@@ -703,18 +743,22 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
   using CF = tc::Cfg<BN, MODE>;
   TcMaps maps;
   // A: M x K (TA: stored K x M); B: K x N (TB: stored N x K)
-  int rc = op_maps(A, TA, M, K, tc::BM, n, MODE == 3, &maps.a_hi, &maps.a_lo);
+  const int tn = (N + BN - 1) / BN, tm = (M + tc::BM - 1) / tc::BM;
+  const long long tiles = (long long)tn * tm * n * ks;
+  static const int persist = getenv("SKG_GEMM_PERSIST") ? atoi(getenv("SKG_GEMM_PERSIST")) : 1;
+  const bool use_p = persist && tiles >= 3LL * sm_count();
+  // MN-major operands in one 4D box per stage (k_gemm_tc only; SKG_GEMM_TMA4=0: per block)
+  static const int tma4_on = getenv("SKG_GEMM_TMA4") ? atoi(getenv("SKG_GEMM_TMA4")) : 1;
+  const bool blk = tma4_on && !use_p;
+  int rc = op_maps(A, TA, M, K, tc::BM, n, MODE == 3, &maps.a_hi, &maps.a_lo, blk, &maps.a_blk);
   if (rc) return rc;
-  rc = op_maps(B, !TB, N, K, BN, n, MODE == 3, &maps.b_hi, &maps.b_lo);
+  rc = op_maps(B, !TB, N, K, BN, n, MODE == 3, &maps.b_hi, &maps.b_lo, blk, &maps.b_blk);
   if (rc) return rc;
   maps.c_tma = 0;
   static const int early = getenv("SKG_GEMM_EARLY") ? atoi(getenv("SKG_GEMM_EARLY")) : 1;
   maps.early = early;
   const int as = A.stride ? n : 1, bs = B.stride ? n : 1;
-  const int tn = (N + BN - 1) / BN, tm = (M + tc::BM - 1) / tc::BM;
-  const long long tiles = (long long)tn * tm * n * ks;
-  static const int persist = getenv("SKG_GEMM_PERSIST") ? atoi(getenv("SKG_GEMM_PERSIST")) : 1;
-  if (persist && tiles >= 3LL * sm_count()) {
+  if (use_p) {
     // >= 3 waves (GraphSAINT's 36K-row GEMMs): persistent CTAs with double-buffered TMEM
     // accumulators.  Not for shorter grids: persistent CTAs hold every SM until the GEMM
     // ends, which starves the concurrent sampler streams (YouTube step: 1720 vs 1808 it/s
@@ -739,7 +783,7 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
   const int64_t nz = (int64_t)n * ks;
   if (tma_store && !acc && C.ld % 4 == 0 && (reinterpret_cast<uintptr_t>(C.base) & 15) == 0 &&
       (nz == 1 || (C.stride % 4 == 0 && C.stride >= C.ld * (int64_t)M)) &&
-      get_map(C.base, N, M, nz, C.ld, nz == 1 ? 0 : C.stride, tc::BM, false, &maps.c) == SKG_OK)
+      get_map(C.base, N, M, nz, C.ld, nz == 1 ? 0 : C.stride, tc::BM, 0, &maps.c) == SKG_OK)
     maps.c_tma = 1;
   auto kern = k_gemm_tc<TA, TB, BN, MODE>;
   static bool attr = false;
