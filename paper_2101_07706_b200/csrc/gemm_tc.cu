@@ -471,13 +471,17 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
             uint8_t* sb = sa + CF::A_BYTES;
             const CUtensorMap* ma = part ? &maps.a_lo : &maps.a_hi;
             const CUtensorMap* mb = part ? &maps.b_lo : &maps.b_hi;
-            if (A_MN) {
+            if (A_MN && maps.a_blk) {
+              tma4(sa, ma, 0, k0, m0 / 32, za, &full_bar[s]);
+            } else if (A_MN) {
 #pragma unroll
               for (int i = 0; i < BM / 32; ++i) tma3(sa + i * 4096, ma, m0 + 32 * i, k0, za, &full_bar[s]);
             } else {
               tma3(sa, ma, k0, m0, za, &full_bar[s]);
             }
-            if (B_MN) {
+            if (B_MN && maps.b_blk) {
+              tma4(sb, mb, 0, k0, n0 / 32, zb, &full_bar[s]);
+            } else if (B_MN) {
 #pragma unroll
               for (int i = 0; i < BN / 32; ++i) tma3(sb + i * 4096, mb, n0 + 32 * i, k0, zb, &full_bar[s]);
             } else {
@@ -747,9 +751,10 @@ static int launch_tc(int n, int M, int N, int K, const int32_t* const* dM, const
   const long long tiles = (long long)tn * tm * n * ks;
   static const int persist = getenv("SKG_GEMM_PERSIST") ? atoi(getenv("SKG_GEMM_PERSIST")) : 1;
   const bool use_p = persist && tiles >= 3LL * sm_count();
-  // MN-major operands in one 4D box per stage (k_gemm_tc only; SKG_GEMM_TMA4=0: per block)
+  // MN-major operands in one 4D box per stage (SKG_GEMM_TMA4=0: per block; =2: not in the
+  // persistent kernel)
   static const int tma4_on = getenv("SKG_GEMM_TMA4") ? atoi(getenv("SKG_GEMM_TMA4")) : 1;
-  const bool blk = tma4_on && !use_p;
+  const bool blk = tma4_on == 1 || (tma4_on == 2 && !use_p);
   int rc = op_maps(A, TA, M, K, tc::BM, n, MODE == 3, &maps.a_hi, &maps.a_lo, blk, &maps.a_blk);
   if (rc) return rc;
   rc = op_maps(B, !TB, N, K, BN, n, MODE == 3, &maps.b_hi, &maps.b_lo, blk, &maps.b_blk);
