@@ -140,7 +140,7 @@ struct TcMaps {
   CUtensorMap a_hi, a_lo, b_hi, b_lo;
   CUtensorMap c;  // output boxes {32 columns, 128 rows, 1 block} for the TMA-store epilogue
   int c_tma;      // 1: the epilogue stages the tile in shared memory and stores it by TMA
-  int early;      // 1: stage 0's TMA loads are issued before the setup sync (k_gemm_tc)
+  int early;      // chunks whose TMA loads are issued before the setup sync (k_gemm_tc; <= STAGES)
   int a_blk, b_blk;  // 1: the MN-major operand's 32-wide blocks come in one 4D box (k_gemm_tc)
 };
 
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
     mbar_init(&done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;");
     // the first chunk's loads fly while TMEM is allocated and the CTA synchronises
-    if (maps.early && nk > 0) load_stage(0);
+    for (int kc = 0; kc < maps.early && kc < nk && kc < STAGES; ++kc) load_stage(kc);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(tc::NTHREADS, 1)
   if (warp == 0) {
     // ---------------- TMA producer
     if (lane == 0) {
-      for (int kc = maps.early ? 1 : 0; kc < nk; ++kc) {
+      for (int kc = min(maps.early, STAGES); kc < nk; ++kc) {
         const int s = kc % STAGES;
         if (kc >= STAGES) mbar_wait(&empty_bar[s], (uint32_t)(((kc / STAGES) - 1) & 1));
         load_stage(kc);
